@@ -1,0 +1,183 @@
+/*
+ * synchro_b200.h — C-ABI of the B200-native exact reset-threshold search.
+ *
+ * Drop-in boundary for the reference's C++ API (/root/reference/proj/include/
+ * synchro/ headers) and CLI (proj/tools/synchro.cpp).  Plain pointers and sizes
+ * only; no CUDA or torch types.  Every entry point returns an int status:
+ *
+ *   SW_OK                     0
+ *   SW_ERR_OTHER              1  std::logic_error etc.         (CLI exit 1)
+ *   SW_ERR_NOT_SYNCHRONIZING  2  NotSynchronizingError          (CLI exit 2)
+ *   SW_ERR_PARSE              3  ParseError / invalid_argument  (CLI exit 3)
+ *   SW_ERR_OUT_OF_MEMORY      4  OutOfMemoryError (ledger)      (CLI exit 4)
+ *   SW_ERR_REFUSED            5  oracle n > 20                  (CLI exit 5)
+ *   SW_ERR_TIMEOUT            6  TimeoutError                   (CLI exit 6)
+ *   SW_ERR_DEVICE            10  CUDA failure / no device (no CPU fallback)
+ *
+ * and sw_last_error() returns the message of the calling thread's last failure.
+ * Automata are (n, k, delta) with delta row-major: delta[q*k + a]
+ * (automaton.hpp:20-45).  Set lists are words[count][W] u64 with
+ * W = ceil(n/64), MSB-first packing (state 0 = bit 63 of word 0,
+ * state_set.hpp:14-19), plus u32 cards and optional u64 tags.
+ */
+#ifndef SYNCHRO_B200_H_
+#define SYNCHRO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW_OK 0
+#define SW_ERR_OTHER 1
+#define SW_ERR_NOT_SYNCHRONIZING 2
+#define SW_ERR_PARSE 3
+#define SW_ERR_OUT_OF_MEMORY 4
+#define SW_ERR_REFUSED 5
+#define SW_ERR_TIMEOUT 6
+#define SW_ERR_DEVICE 10
+
+/* Schedule (bibfs_engine.hpp:20-25) */
+#define SW_SCHEDULE_AUTO 0
+#define SW_SCHEDULE_BFS 1
+#define SW_SCHEDULE_IBFS 2
+#define SW_SCHEDULE_DFS 3
+
+/* StepKind (cost_model.hpp:13) */
+#define SW_STEP_BFS 0
+#define SW_STEP_BFS_NH 1
+#define SW_STEP_IBFS 2
+#define SW_STEP_IBFS_NH 3
+#define SW_STEP_DFS 4
+
+/* SolveOptions + EngineTuning + TuningParams (bibfs_engine.hpp:27-48,
+ * cost_model.hpp:26-36), flattened.  Use sw_default_options(). */
+typedef struct sw_solve_options {
+  uint64_t memory;          /* ledger budget in bytes (default 4 GiB) */
+  double time_limit;        /* seconds, <= 0: none */
+  int32_t track_word;       /* reconstruct and return a shortest reset word */
+  int32_t schedule;         /* SW_SCHEDULE_* */
+  uint64_t upper_bound;     /* 0: run the adaptive heuristic */
+  double set_cost;          /* 512 */
+  double dfs_set_weight;    /* 0.25 */
+  double dfs_check_weight;  /* 0.25 */
+  uint32_t min_brute;       /* 64 (performance-only in the reference) */
+  uint32_t min_leaf;        /* 10 */
+  uint32_t dedupe_cadence;  /* 2 */
+  uint32_t reduce_cadence;  /* 3 */
+  int32_t device;           /* CUDA device, -1: current */
+  int32_t timing;           /* 1: time expansion kernels with CUDA events */
+} sw_solve_options;
+
+/* SolveResult (bibfs_engine.hpp:50-59) + expansion counters and timings. */
+typedef struct sw_solve_result {
+  uint64_t threshold;
+  uint64_t upper_bound;
+  uint64_t iterations;
+  uint64_t bfs_steps;
+  uint64_t ibfs_steps;
+  uint64_t peak_memory;
+  int32_t used_dfs;
+  int32_t has_word;
+  uint64_t word_len;
+  uint64_t expansions_phase1;
+  uint64_t expansions_dfs;
+  double heuristic_seconds;
+  double engine_seconds;
+  double expand_kernel_ms;
+  uint64_t kernel_launches;
+  char phase[16];           /* "meet" | "dfs" | "bound" | "trivial" */
+} sw_solve_result;
+
+const char* sw_version(void);
+const char* sw_last_error(void);
+int sw_device_count(void);
+void sw_default_options(sw_solve_options* opt);
+
+/* ---- automata (automaton.hpp:159-219, experiment.hpp:54-56) ---- */
+int sw_random_automaton(uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta_out);
+int sw_cerny_automaton(uint32_t n, uint32_t* delta_out);
+uint64_t sw_instance_seed(uint64_t seed_base, uint32_t n, uint32_t index);
+/* Text format "n k" then n rows of k targets; '#' comments.  Pass delta_out =
+ * NULL to query n and k first. */
+int sw_parse_automaton(const char* text, uint32_t* n, uint32_t* k, uint32_t* delta_out,
+                       size_t delta_cap);
+int sw_is_synchronizing(uint32_t n, uint32_t k, const uint32_t* delta, int32_t* result);
+int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, const uint32_t* word,
+                     size_t len, int32_t* result);
+
+/* ---- exact search: replaces synchro::solve_exact (bibfs_engine.hpp:467) ----
+ * word: caller buffer of word_cap letters (may be NULL); trace_path: file for
+ * the per-iteration trace (bibfs_engine.hpp:442-460) or NULL. */
+int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta, const sw_solve_options* opt,
+                   sw_solve_result* result, uint32_t* word, size_t word_cap,
+                   const char* trace_path);
+
+/* ---- heuristics (heuristics.hpp:26-184) ----
+ * algorithm: 0 eppstein, 1 beam, 2 adaptive.  Returns SW_ERR_REFUSED when the
+ * beam finds no reset word (CLI exit 5). */
+int sw_heuristic(uint32_t n, uint32_t k, const uint32_t* delta, int32_t algorithm,
+                 uint64_t beam_size, uint64_t memory, double time_limit, uint64_t* bound,
+                 uint32_t* word, size_t word_cap);
+
+/* ---- power-set BFS oracle (oracle.hpp:17), n <= 20 ---- */
+int sw_power_set_oracle(uint32_t n, uint32_t k, const uint32_t* delta, double time_limit,
+                        uint64_t* threshold);
+
+/* ---- engine handle (replaces detail::BibfsEngine, bibfs_engine.hpp:66-440) ---- */
+typedef struct sw_engine sw_engine;
+typedef struct sw_engine_stats {
+  uint64_t iteration, bound;
+  uint64_t lbfs, libfs, hbfs, hibfs;  /* list sizes */
+  double d_lbfs, d_libfs;            /* densities */
+  uint64_t ledger_used, ledger_peak;
+} sw_engine_stats;
+int sw_engine_create(uint32_t n, uint32_t k, const uint32_t* delta, const sw_solve_options* opt,
+                     uint64_t upper_bound, sw_engine** out);
+int sw_engine_destroy(sw_engine* eng);
+/* Cost-model choice for iteration r (make_stats + compute_step_costs + select_step). */
+int sw_engine_choose(sw_engine* eng, uint64_t r, int32_t* kind);
+int sw_engine_step(sw_engine* eng, int32_t kind);      /* SW_STEP_BFS..IBFS_NH */
+int sw_engine_meet(sw_engine* eng, int32_t* met);
+int sw_engine_dfs(sw_engine* eng, uint64_t r, uint64_t* threshold);
+int sw_engine_stats_get(sw_engine* eng, sw_engine_stats* out);
+
+/* ---- data-plane primitives on host buffers (parity tests; set_list.hpp,
+ * subset_algebra.hpp, static_trie.hpp).  Each uploads, runs the B200 kernel(s)
+ * and downloads. ---- */
+/* out_* hold count*k children, child o = i*k + a (bibfs_engine.hpp:345-367). */
+int sw_list_expand(uint32_t n, uint32_t k, const uint32_t* delta, const uint64_t* words,
+                   size_t count, int32_t inverse, uint64_t* out_words, uint32_t* out_cards);
+/* In place; *out_count = surviving count.  tags may be NULL. */
+int sw_list_lex_sort_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                            size_t count, size_t* out_count);
+int sw_list_sort_card_desc_lex(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                               size_t count);
+int sw_list_dedupe_sorted(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                          size_t count, size_t* out_count);
+int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards, size_t count,
+                                size_t* out_count);
+/* keep[j] = 1 iff b[j] is NOT marked.  mode 0: supersets (incl. equal),
+ * 1: proper supersets, 2: subsets.  a must be lex-sorted unique for modes 0/1
+ * (require_sorted_unique, subset_algebra.hpp:127-130) else SW_ERR_PARSE. */
+int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count, const uint64_t* b_words,
+                 size_t b_count, int32_t mode, uint8_t* keep);
+int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
+                       const uint64_t* b_words, size_t b_count, int32_t* met);
+/* Node count of the reference StaticTrie over a duplicate-free list. */
+int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t min_leaf,
+                       uint64_t* nodes);
+
+/* ---- experiment runner (experiment.hpp:133-188) → CSV file ---- */
+int sw_run_experiment(const uint32_t* ns, size_t ns_count, uint32_t k, uint32_t samples,
+                      uint64_t seed_base, const char* solver, double time_limit, uint64_t memory,
+                      uint32_t threads, int32_t deterministic, uint32_t shard_index,
+                      uint32_t shard_count, const char* csv_path);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SYNCHRO_B200_H_ */

@@ -1,0 +1,444 @@
+// C-ABI (include/synchro_b200.h): exceptions → status codes, host buffers in
+// and out.  Every entry point maps the reference's exception classes onto the
+// CLI exit codes (tools/synchro.cpp:325-344).
+#include "../../include/synchro_b200.h"
+
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "device/dev.hpp"
+#include "engine.hpp"
+#include "experiment.hpp"
+
+#define SW_EXPORT extern "C" __attribute__((visibility("default")))
+
+using namespace synchro;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return SW_OK;
+  } catch (const NotSynchronizingError& e) {
+    g_last_error = e.what();
+    return SW_ERR_NOT_SYNCHRONIZING;
+  } catch (const ParseError& e) {
+    g_last_error = e.what();
+    return SW_ERR_PARSE;
+  } catch (const OutOfMemoryError& e) {
+    g_last_error = e.what();
+    return SW_ERR_OUT_OF_MEMORY;
+  } catch (const TimeoutError& e) {
+    g_last_error = e.what();
+    return SW_ERR_TIMEOUT;
+  } catch (const DeviceError& e) {
+    g_last_error = e.what();
+    return SW_ERR_DEVICE;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return SW_ERR_PARSE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SW_ERR_OTHER;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return SW_ERR_OTHER;
+  }
+}
+
+Automaton make_aut(uint32_t n, uint32_t k, const uint32_t* delta) {
+  if (!delta) throw std::invalid_argument("delta is NULL");
+  return Automaton(n, k, std::vector<u32>(delta, delta + static_cast<size_t>(n) * k));
+}
+
+// A context for list primitives that need no transition table.
+Automaton identity_aut(uint32_t n) {
+  std::vector<u32> d(n);
+  for (u32 q = 0; q < n; ++q) d[q] = q;
+  return Automaton(n, 1, std::move(d));
+}
+
+SolveOptions to_options(const sw_solve_options* o) {
+  sw_solve_options def;
+  sw_default_options(&def);
+  if (!o) o = &def;
+  SolveOptions s;
+  s.memory = o->memory;
+  if (o->time_limit > 0) s.time_limit = o->time_limit;
+  s.track_word = o->track_word != 0;
+  switch (o->schedule) {
+    case SW_SCHEDULE_AUTO: s.schedule = Schedule::Auto; break;
+    case SW_SCHEDULE_BFS: s.schedule = Schedule::BfsOnly; break;
+    case SW_SCHEDULE_IBFS: s.schedule = Schedule::IbfsOnly; break;
+    case SW_SCHEDULE_DFS: s.schedule = Schedule::DfsImmediate; break;
+    default: throw std::invalid_argument("unknown schedule");
+  }
+  if (o->upper_bound) s.upper_bound = o->upper_bound;
+  s.tuning.cost.set_cost = o->set_cost;
+  s.tuning.cost.dfs_set_cost_weight = o->dfs_set_weight;
+  s.tuning.cost.dfs_check_cost_weight = o->dfs_check_weight;
+  s.tuning.min_brute = o->min_brute;
+  s.tuning.min_leaf = o->min_leaf;
+  s.tuning.dfs_dedupe_cadence = o->dedupe_cadence;
+  s.tuning.dfs_reduce_cadence = o->reduce_cadence;
+  s.device = o->device;
+  s.timing = o->timing != 0;
+  return s;
+}
+
+bool sorted_unique(const uint64_t* w, size_t count, u32 W) {
+  for (size_t i = 1; i < count; ++i)
+    if (!std::lexicographical_compare(w + (i - 1) * W, w + i * W, w + i * W, w + (i + 1) * W))
+      return false;
+  return true;
+}
+
+}  // namespace
+
+struct sw_engine {
+  Automaton aut;
+  SolveOptions opt;
+  std::unique_ptr<dev::Context> ctx;
+  std::unique_ptr<detail::GpuBibfs> eng;
+};
+
+SW_EXPORT const char* sw_version(void) { return "synchro-b200 0.1 (sm_100a)"; }
+SW_EXPORT const char* sw_last_error(void) { return g_last_error.c_str(); }
+SW_EXPORT int sw_device_count(void) { return dev::device_count(); }
+
+SW_EXPORT void sw_default_options(sw_solve_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->memory = u64{4} << 30;
+  o->schedule = SW_SCHEDULE_AUTO;
+  o->set_cost = 512.0;
+  o->dfs_set_weight = 0.25;
+  o->dfs_check_weight = 0.25;
+  o->min_brute = 64;
+  o->min_leaf = 10;
+  o->dedupe_cadence = 2;
+  o->reduce_cadence = 3;
+  o->device = -1;
+}
+
+SW_EXPORT int sw_random_automaton(uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta_out) {
+  return guarded([&] {
+    const Automaton a = random_automaton(n, k, seed);
+    std::memcpy(delta_out, a.table().data(), a.table().size() * 4);
+  });
+}
+
+SW_EXPORT int sw_cerny_automaton(uint32_t n, uint32_t* delta_out) {
+  return guarded([&] {
+    const Automaton a = cerny_automaton(n);
+    std::memcpy(delta_out, a.table().data(), a.table().size() * 4);
+  });
+}
+
+SW_EXPORT uint64_t sw_instance_seed(uint64_t base, uint32_t n, uint32_t index) {
+  return instance_seed(base, n, index);
+}
+
+SW_EXPORT int sw_parse_automaton(const char* text, uint32_t* n, uint32_t* k, uint32_t* delta_out,
+                                 size_t cap) {
+  return guarded([&] {
+    const Automaton a = parse_automaton(std::string(text ? text : ""));
+    *n = a.state_count();
+    *k = a.alphabet_size();
+    if (delta_out) {
+      if (cap < a.table().size()) throw std::invalid_argument("delta buffer too small");
+      std::memcpy(delta_out, a.table().data(), a.table().size() * 4);
+    }
+  });
+}
+
+SW_EXPORT int sw_is_synchronizing(uint32_t n, uint32_t k, const uint32_t* delta, int32_t* result) {
+  return guarded([&] { *result = is_synchronizing(make_aut(n, k, delta)) ? 1 : 0; });
+}
+
+SW_EXPORT int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, const uint32_t* word,
+                               size_t len, int32_t* result) {
+  return guarded([&] {
+    *result = is_reset_word(make_aut(n, k, delta), Word(word, word + len)) ? 1 : 0;
+  });
+}
+
+SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
+                             const sw_solve_options* o, sw_solve_result* out, uint32_t* word,
+                             size_t word_cap, const char* trace_path) {
+  return guarded([&] {
+    std::memset(out, 0, sizeof(*out));
+    const Automaton aut = make_aut(n, k, delta);
+    SolveOptions opt = to_options(o);
+    std::ofstream trace;
+    if (trace_path && *trace_path) {
+      trace.open(trace_path);
+      if (!trace) throw ParseError(std::string("cannot open ") + trace_path);
+      opt.trace = &trace;
+    }
+    const SolveResult r = solve_exact(aut, opt);
+    out->threshold = r.threshold;
+    out->upper_bound = r.upper_bound;
+    out->iterations = r.iterations;
+    out->bfs_steps = r.bfs_steps;
+    out->ibfs_steps = r.ibfs_steps;
+    out->peak_memory = r.peak_memory;
+    out->used_dfs = r.used_dfs ? 1 : 0;
+    out->has_word = r.word ? 1 : 0;
+    out->word_len = r.word ? r.word->size() : 0;
+    out->expansions_phase1 = r.expansions_phase1;
+    out->expansions_dfs = r.expansions_dfs;
+    out->heuristic_seconds = r.heuristic_seconds;
+    out->engine_seconds = r.engine_seconds;
+    out->expand_kernel_ms = r.expand_kernel_ms;
+    out->kernel_launches = r.kernel_launches;
+    std::strncpy(out->phase, r.phase.c_str(), sizeof(out->phase) - 1);
+    if (r.word && word)
+      for (size_t i = 0; i < r.word->size() && i < word_cap; ++i) word[i] = (*r.word)[i];
+  });
+}
+
+SW_EXPORT int sw_heuristic(uint32_t n, uint32_t k, const uint32_t* delta, int32_t algorithm,
+                           uint64_t beam_size, uint64_t memory, double time_limit, uint64_t* bound,
+                           uint32_t* word, size_t word_cap) {
+  int refused = 0;
+  const int rc = guarded([&] {
+    const Automaton aut = make_aut(n, k, delta);
+    if (!is_synchronizing(aut)) throw NotSynchronizingError();
+    const Deadline dl = time_limit > 0 ? Deadline::after_seconds(time_limit) : Deadline();
+    HeuristicResult res;
+    if (algorithm == 0) {
+      res = eppstein(aut, dl);
+    } else if (algorithm == 1) {
+      const u64 beam = beam_size ? beam_size : std::max<u64>(64, n);
+      auto b = beam_ibfs(aut, beam, dl);
+      if (!b) {
+        refused = 1;
+        g_last_error = "beam search found no reset word at beam size " + std::to_string(beam);
+        return;
+      }
+      res = std::move(*b);
+    } else {
+      AdaptiveOptions a;
+      a.memory = memory;
+      a.deadline = dl;
+      if (n == 1) {
+        res = eppstein(aut, dl);
+      } else {
+        dev::Context ctx(aut);
+        res = adaptive_upper_bound(aut, a, &ctx);
+      }
+    }
+    if (!is_reset_word(aut, res.word)) throw std::logic_error("invalid word");
+    *bound = res.length;
+    if (word)
+      for (size_t i = 0; i < res.word.size() && i < word_cap; ++i) word[i] = res.word[i];
+  });
+  if (rc == SW_OK && refused) return SW_ERR_REFUSED;
+  return rc;
+}
+
+SW_EXPORT int sw_power_set_oracle(uint32_t n, uint32_t k, const uint32_t* delta, double time_limit,
+                                  uint64_t* threshold) {
+  const Automaton* dummy = nullptr;
+  (void)dummy;
+  if (n > kOracleMaxStates) {
+    g_last_error = "oracle refuses n > 20";
+    return SW_ERR_REFUSED;
+  }
+  return guarded([&] {
+    const Deadline dl = time_limit > 0 ? Deadline::after_seconds(time_limit) : Deadline();
+    *threshold = power_set_bfs_oracle(make_aut(n, k, delta), dl);
+  });
+}
+
+// ---------------------------------------------------------------- engine
+SW_EXPORT int sw_engine_create(uint32_t n, uint32_t k, const uint32_t* delta,
+                               const sw_solve_options* o, uint64_t upper_bound, sw_engine** out) {
+  return guarded([&] {
+    auto e = std::unique_ptr<sw_engine>(new sw_engine{make_aut(n, k, delta), to_options(o), {}, {}});
+    e->opt.trace = nullptr;
+    e->ctx = std::make_unique<dev::Context>(e->aut, e->opt.device);
+    e->eng = std::make_unique<detail::GpuBibfs>(e->aut, upper_bound, e->opt, *e->ctx);
+    *out = e.release();
+  });
+}
+
+SW_EXPORT int sw_engine_destroy(sw_engine* e) {
+  return guarded([&] {
+    if (!e) return;
+    e->eng.reset();
+    e->ctx.reset();
+    delete e;
+  });
+}
+
+SW_EXPORT int sw_engine_choose(sw_engine* e, uint64_t r, int32_t* kind) {
+  return guarded([&] {
+    e->eng->set_iteration(r);
+    const StepCosts sc = compute_step_costs(e->eng->make_stats(), e->opt.tuning.cost);
+    *kind = static_cast<int32_t>(select_step(sc));
+  });
+}
+
+SW_EXPORT int sw_engine_step(sw_engine* e, int32_t kind) {
+  return guarded([&] {
+    if (kind < 0 || kind > 3) throw std::invalid_argument("not a list step");
+    e->eng->perform(static_cast<StepKind>(kind));
+  });
+}
+
+SW_EXPORT int sw_engine_meet(sw_engine* e, int32_t* met) {
+  return guarded([&] { *met = e->eng->meet() ? 1 : 0; });
+}
+
+SW_EXPORT int sw_engine_dfs(sw_engine* e, uint64_t r, uint64_t* threshold) {
+  return guarded([&] { *threshold = e->eng->run_dfs(r, nullptr, nullptr, nullptr); });
+}
+
+SW_EXPORT int sw_engine_stats_get(sw_engine* e, sw_engine_stats* out) {
+  return guarded([&] {
+    const SearchStats s = e->eng->make_stats();
+    out->iteration = e->eng->iteration();
+    out->bound = e->eng->bound();
+    out->lbfs = static_cast<uint64_t>(s.bfs.list_size);
+    out->libfs = static_cast<uint64_t>(s.ibfs.list_size);
+    out->hbfs = static_cast<uint64_t>(s.bfs.hist_size);
+    out->hibfs = static_cast<uint64_t>(s.ibfs.hist_size);
+    out->d_lbfs = s.bfs.list_density;
+    out->d_libfs = s.ibfs.list_density;
+    out->ledger_used = e->eng->ledger().used();
+    out->ledger_peak = e->eng->ledger().peak();
+  });
+}
+
+// -------------------------------------------------------------- primitives
+SW_EXPORT int sw_list_expand(uint32_t n, uint32_t k, const uint32_t* delta, const uint64_t* words,
+                             size_t count, int32_t inverse, uint64_t* out_words,
+                             uint32_t* out_cards) {
+  return guarded([&] {
+    const Automaton aut = make_aut(n, k, delta);
+    dev::Context c(aut);
+    dev::DList src = dev::upload(c, words, nullptr, nullptr, count);
+    dev::DList out(&c, count * k, false);
+    dev::expand(c, src, 0, count, inverse != 0, out);
+    dev::download(c, out, out_words, out_cards, nullptr);
+  });
+}
+
+namespace {
+template <class Op>
+int list_op(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags, size_t count,
+            size_t* out_count, Op op) {
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    dev::DList l = dev::upload(c, words, cards, tags, count);
+    op(c, l);
+    dev::download(c, l, words, cards, tags);
+    if (out_count) *out_count = l.size();
+  });
+}
+}  // namespace
+
+SW_EXPORT int sw_list_lex_sort_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                                      size_t count, size_t* out_count) {
+  return list_op(n, words, cards, tags, count, out_count,
+                 [](dev::Context& c, dev::DList& l) { dev::lex_sort_dedupe(c, l); });
+}
+
+SW_EXPORT int sw_list_sort_card_desc_lex(uint32_t n, uint64_t* words, uint32_t* cards,
+                                         uint64_t* tags, size_t count) {
+  return list_op(n, words, cards, tags, count, nullptr,
+                 [](dev::Context& c, dev::DList& l) { dev::sort_card_desc_lex(c, l); });
+}
+
+SW_EXPORT int sw_list_dedupe_sorted(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                                    size_t count, size_t* out_count) {
+  return list_op(n, words, cards, tags, count, out_count,
+                 [](dev::Context& c, dev::DList& l) { dev::dedupe_sorted(c, l); });
+}
+
+SW_EXPORT int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards,
+                                          size_t count, size_t* out_count) {
+  if (!sorted_unique(words, count, words_for(n))) {
+    g_last_error = "self_reduce_minimal: first list must be lex-sorted and unique";
+    return SW_ERR_PARSE;
+  }
+  return list_op(n, words, cards, nullptr, count, out_count,
+                 [](dev::Context& c, dev::DList& l) { dev::self_reduce_minimal(c, l); });
+}
+
+SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
+                           const uint64_t* b_words, size_t b_count, int32_t mode, uint8_t* keep) {
+  if (mode != 2 && !sorted_unique(a_words, a_count, words_for(n))) {
+    g_last_error = "mark_supersets: first list must be lex-sorted and unique";
+    return SW_ERR_PARSE;
+  }
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
+    dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    if (mode == 2) {  // subsets of a ⟺ supersets among complements
+      dev::complement(c, a);
+      dev::lex_sort_dedupe(c, a);
+      dev::complement(c, b);
+    }
+    const dev::ContainIndex ix = dev::build_index(c, a);
+    const std::vector<uint8_t> k = dev::superset_keep(c, a, ix, b, mode == 1);
+    std::memcpy(keep, k.data(), k.size());
+  });
+}
+
+SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
+                                 const uint64_t* b_words, size_t b_count, int32_t* met) {
+  if (!sorted_unique(a_words, a_count, words_for(n))) {
+    g_last_error = "meet_check: first list must be lex-sorted and unique";
+    return SW_ERR_PARSE;
+  }
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
+    dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    const dev::ContainIndex ix = dev::build_index(c, a);
+    *met = dev::exists_subset(c, a, ix, b, nullptr) ? 1 : 0;
+  });
+}
+
+SW_EXPORT int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t min_leaf,
+                                 uint64_t* nodes) {
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    dev::DList l = dev::upload(c, words, nullptr, nullptr, count);
+    *nodes = dev::trie_node_count(c, l, min_leaf);
+  });
+}
+
+SW_EXPORT int sw_run_experiment(const uint32_t* ns, size_t ns_count, uint32_t k, uint32_t samples,
+                                uint64_t seed_base, const char* solver, double time_limit,
+                                uint64_t memory, uint32_t threads, int32_t deterministic,
+                                uint32_t shard_index, uint32_t shard_count, const char* csv_path) {
+  return guarded([&] {
+    ExperimentSpec spec;
+    spec.ns.assign(ns, ns + ns_count);
+    spec.k = k;
+    spec.samples = samples;
+    spec.seed_base = seed_base;
+    spec.solver = solver ? solver : "exact";
+    spec.time_limit = time_limit > 0 ? std::optional<double>(time_limit) : std::nullopt;
+    spec.memory = memory;
+    spec.threads = threads;
+    spec.deterministic = deterministic != 0;
+    spec.shard_index = shard_index;
+    spec.shard_count = shard_count ? shard_count : 1;
+    std::ofstream out(csv_path);
+    if (!out) throw ParseError(std::string("cannot open ") + csv_path);
+    run_experiment(spec, out, nullptr);
+  });
+}

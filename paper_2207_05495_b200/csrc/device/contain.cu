@@ -1,0 +1,294 @@
+// Subset-containment on the GPU: the B200 replacement for the reference's
+// MarkSupersets recursion (subset_algebra.hpp:55-125, Alg. 2) and for the
+// static-trie joint query (static_trie.hpp:153-188).
+//
+// The reference splits a lex-sorted A on bit d by binary search and
+// partitions B in place, recursively — inherently sequential.  Here the
+// lex-sorted unique A is turned into an explicit binary radix (Patricia) tree
+// in parallel (Karras, HPG 2012: node i of N-1 internal nodes is found from
+// longest-common-prefix lengths of neighbouring keys by binary search, no
+// inter-thread communication), each node annotated with its subtree's
+// minimum cardinality.  Every query set y is then handled by one thread that
+// walks the tree depth-first:
+//   * a node's keys agree on bits < lcp; bits [d, lcp) of that common prefix
+//     must lie in y (else the subtree is dead);
+//   * at the split bit L the 0-child is always admissible, the 1-child only if
+//     y has state L (exactly the reference's "ones side recurses with B_1");
+//   * subtrees whose min cardinality exceeds |y| (|y|-1 for proper) are cut —
+//     the reference's per-pair card filter lifted to whole subtrees;
+//   * ranges of <= kBrute keys are scanned linearly (contiguous rows).
+// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} is independent of
+// traversal order, so sizes match the reference bit-exactly.
+#include <cub/cub.cuh>
+
+#include "dev.hpp"
+#include "kernels.cuh"
+#include "util.cuh"
+
+namespace synchro::dev {
+
+struct __align__(16) Node {
+  u32 first, last;  // key range [first, last]
+  u32 split;        // left = [first, split], right = [split+1, last]
+  uint16_t lcp;     // first bit where the range's keys differ
+  uint16_t minc;    // min cardinality in the range
+};
+
+constexpr u32 kLeafBit = 0x80000000u;
+constexpr int kBrute = 12;
+constexpr int kStack = 64;
+
+template <int W>
+__device__ __forceinline__ int key_delta(const u64* __restrict__ A, long long N, long long i,
+                                         long long j) {
+  if (j < 0 || j >= N) return -1;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const u64 x = A[i * W + w] ^ A[j * W + w];
+    if (x) return w * 64 + __clzll(x);
+  }
+  return W * 64;
+}
+
+template <int W>
+__global__ void karras_kernel(const u64* __restrict__ A, u32 N, Node* __restrict__ nodes,
+                              u32* __restrict__ parent_int, u32* __restrict__ parent_leaf) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(N) - 1) return;
+  const int dn = key_delta<W>(A, N, i, i + 1), dp = key_delta<W>(A, N, i, i - 1);
+  const int d = dn > dp ? 1 : -1;
+  const int dmin = dn > dp ? dp : dn;
+  long long lmax = 2;
+  while (key_delta<W>(A, N, i, i + lmax * d) > dmin) lmax <<= 1;
+  long long l = 0;
+  for (long long t = lmax >> 1; t >= 1; t >>= 1)
+    if (key_delta<W>(A, N, i, i + (l + t) * d) > dmin) l += t;
+  const long long j = i + l * d;
+  const int dnode = key_delta<W>(A, N, i, j);
+  long long s = 0, t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (key_delta<W>(A, N, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  const long long gamma = i + s * d + (d < 0 ? -1 : 0);
+  const u32 first = static_cast<u32>(i < j ? i : j), last = static_cast<u32>(i < j ? j : i);
+  Node nd;
+  nd.first = first;
+  nd.last = last;
+  nd.split = static_cast<u32>(gamma);
+  nd.lcp = static_cast<uint16_t>(dnode);
+  nd.minc = 0xFFFF;
+  nodes[i] = nd;
+  if (first == gamma) parent_leaf[gamma] = static_cast<u32>(i);
+  else parent_int[gamma] = static_cast<u32>(i);
+  if (last == gamma + 1) parent_leaf[gamma + 1] = static_cast<u32>(i);
+  else parent_int[gamma + 1] = static_cast<u32>(i);
+}
+
+// Bottom-up min cardinality: the second child to arrive at a node finishes it.
+__global__ void mincard_kernel(const u32* __restrict__ card, u32 N, Node* nodes,
+                               const u32* __restrict__ parent_int,
+                               const u32* __restrict__ parent_leaf, u32* arrivals) {
+  const u32 leaf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= N) return;
+  u32 p = parent_leaf[leaf];
+  while (true) {
+    __threadfence();
+    if (atomicAdd(&arrivals[p], 1u) == 0) return;
+    __threadfence();
+    volatile Node* vn = nodes;
+    const u32 first = vn[p].first, last = vn[p].last, split = vn[p].split;
+    const u32 lm = (split == first) ? card[first] : vn[split].minc;
+    const u32 rm = (split + 1 == last) ? card[last] : vn[split + 1].minc;
+    vn[p].minc = static_cast<uint16_t>(lm < rm ? lm : rm);
+    if (p == 0) return;
+    p = parent_int[p];
+  }
+}
+
+ContainIndex build_index(Context& c, const DList& a) {
+  ContainIndex ix;
+  ix.ctx = &c;
+  ix.count = a.size();
+  if (a.size() < 2) return ix;
+  const u32 N = static_cast<u32>(a.size());
+  cudaStream_t s = as_stream(c.stream());
+  Node* nodes = static_cast<Node*>(c.alloc((N - 1) * sizeof(Node)));
+  u32* pint = static_cast<u32*>(c.alloc(static_cast<size_t>(N) * 4));
+  u32* pleaf = static_cast<u32*>(c.alloc(static_cast<size_t>(N) * 4));
+  u32* arr = static_cast<u32*>(c.alloc(static_cast<size_t>(N) * 4));
+  SW_CUDA(cudaMemsetAsync(arr, 0, static_cast<size_t>(N) * 4, s));
+  SW_DISPATCH_W(c.W(), { karras_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(a.words, N, nodes, pint, pleaf); });
+  mincard_kernel<<<(N + 255) / 256, 256, 0, s>>>(a.cards, N, nodes, pint, pleaf, arr);
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 2;
+  c.free(pint);
+  c.free(pleaf);
+  c.free(arr);
+  ix.nodes = nodes;
+  return ix;
+}
+
+template <int W>
+__device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (&y)[W]) {
+  u64 acc = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) acc |= x[w] & ~y[w];
+  return acc == 0;
+}
+
+// One thread per query y.  EXIST: stop everything at the first hit (meet
+// check / DFS trie query); otherwise write keep[j] = !hit.
+template <int W, bool PROPER, bool EXIST>
+__global__ void __launch_bounds__(128) contain_query_kernel(
+    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
+    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u64 Nb,
+    uint8_t* __restrict__ keep, int* found, unsigned long long* wit) {
+  const u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  if (j >= Nb) return;
+  if (EXIST && *reinterpret_cast<volatile int*>(found)) return;
+  u64 y[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) y[w] = B[j * W + w];
+  const u32 cy = Bcard[j];
+  bool hit = false;
+  u32 hit_a = 0;
+  if (Na > 0 && !(PROPER && cy == 0)) {
+    const u32 limit = PROPER ? cy - 1 : cy;
+    u32 st_id[kStack];
+    uint16_t st_d[kStack];
+    int sp = 0;
+    st_id[sp] = Na == 1 ? kLeafBit : 0u;
+    st_d[sp++] = 0;
+    u32 iter = 0;
+    while (sp > 0 && !hit) {
+      if (EXIST && ((++iter & 63) == 0) && *reinterpret_cast<volatile int*>(found)) break;
+      --sp;
+      const u32 id = st_id[sp];
+      const int d = st_d[sp];
+      if (id & kLeafBit) {
+        const u32 x = id & ~kLeafBit;
+        if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+          hit = true;
+          hit_a = x;
+        }
+        continue;
+      }
+      const Node nd = nodes[id];
+      if (nd.minc > limit) continue;
+      if (nd.last - nd.first < kBrute) {
+        for (u32 x = nd.first; x <= nd.last; ++x)
+          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+            hit = true;
+            hit_a = x;
+            break;
+          }
+        continue;
+      }
+      const int L = nd.lcp;
+      // Bits [d, L) are common to the whole range: they must lie in y.
+      const u64* xf = A + static_cast<u64>(nd.first) * W;
+      u64 bad = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+      if (bad) continue;
+      const u32 left = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+      const u32 right = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+      const bool y_has_L = (y[L >> 6] >> (63 - (L & 63))) & 1;
+      if (sp + 2 > kStack) {
+        // Stack exhausted (very deep tree): finish this subtree linearly.
+        for (u32 x = nd.first; x <= nd.last; ++x)
+          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+            hit = true;
+            hit_a = x;
+            break;
+          }
+        continue;
+      }
+      if (y_has_L) {
+        st_id[sp] = right;
+        st_d[sp++] = static_cast<uint16_t>(L + 1);
+      }
+      st_id[sp] = left;
+      st_d[sp++] = static_cast<uint16_t>(L + 1);
+    }
+  }
+  if (EXIST) {
+    if (hit && atomicCAS(found, 0, 1) == 0) {
+      wit[0] = hit_a;
+      wit[1] = j;
+    }
+  } else {
+    keep[j] = hit ? 0 : 1;
+  }
+}
+
+template <bool PROPER, bool EXIST>
+static void launch_query(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
+                         uint8_t* keep, int* found, unsigned long long* wit) {
+  const u64 Nb = b.size();
+  if (!Nb) return;
+  const int block = 128;
+  const u64 grid = (Nb + block - 1) / block;
+  SW_DISPATCH_W(c.W(), {
+    contain_query_kernel<W, PROPER, EXIST><<<static_cast<unsigned>(grid), block, 0, as_stream(c.stream())>>>(
+        a.words, a.cards, static_cast<const Node*>(ia.nodes), static_cast<u32>(a.size()), b.words,
+        b.cards, Nb, keep, found, wit);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+}
+
+size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper) {
+  if (b.empty() || a.empty()) return 0;
+  const size_t before = b.size();
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+  if (proper)
+    launch_query<true, false>(c, a, ia, b, keep, nullptr, nullptr);
+  else
+    launch_query<false, false>(c, a, ia, b, keep, nullptr, nullptr);
+  return before - compact_flags(c, b, keep, nullptr);
+}
+
+std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
+                                   bool proper) {
+  std::vector<uint8_t> out(b.size(), 1);
+  if (b.empty() || a.empty()) return out;
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+  if (proper)
+    launch_query<true, false>(c, a, ia, b, keep, nullptr, nullptr);
+  else
+    launch_query<false, false>(c, a, ia, b, keep, nullptr, nullptr);
+  c.memcpy_d2h(out.data(), keep, b.size());
+  return out;
+}
+
+size_t self_reduce_minimal(Context& c, DList& l) {
+  if (l.size() <= 1) return 0;
+  const ContainIndex ix = build_index(c, l);
+  const size_t before = l.size();
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
+  launch_query<true, false>(c, l, ix, l, keep, nullptr, nullptr);
+  return before - compact_flags(c, l, keep, nullptr);
+}
+
+bool exists_subset(Context& c, const DList& a, const ContainIndex& ia, const DList& b, Witness* w) {
+  if (a.empty() || b.empty()) return false;
+  struct Res {
+    int found;
+    int pad;
+    unsigned long long wit[2];
+  };
+  auto* d = static_cast<Res*>(c.scratch(7, sizeof(Res)));
+  SW_CUDA(cudaMemsetAsync(d, 0, sizeof(Res), as_stream(c.stream())));
+  launch_query<false, true>(c, a, ia, b, nullptr, &d->found, d->wit);
+  Res h;
+  c.memcpy_d2h(&h, d, sizeof(Res));
+  if (h.found && w) {
+    w->a_index = h.wit[0];
+    w->b_index = h.wit[1];
+  }
+  return h.found != 0;
+}
+
+}  // namespace synchro::dev

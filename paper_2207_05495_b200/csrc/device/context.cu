@@ -1,0 +1,273 @@
+// Device context: stream, stream-ordered memory pool, transition tables,
+// list allocation and host<->device transfer.
+#include <cstring>
+#include <sstream>
+#include <vector>
+
+#include "dev.hpp"
+#include "util.cuh"
+
+namespace synchro::dev {
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  std::ostringstream os;
+  os << "CUDA error " << cudaGetErrorName(e) << " (" << cudaGetErrorString(e) << ") at " << file
+     << ":" << line << " in " << what;
+  throw DeviceError(os.str());
+}
+
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+Context::Context(const Automaton& aut, int device)
+    : n_(aut.state_count()), k_(aut.alphabet_size()), W_(words_for(aut.state_count())) {
+  if (W_ > static_cast<u32>(kMaxW))
+    throw std::invalid_argument("n > 1024 states is not supported by the device kernels");
+  if (static_cast<u64>(n_) * k_ > 24576)
+    throw std::invalid_argument("n*k > 24576 transitions is not supported by the device kernels");
+  int ndev = device_count();
+  if (ndev == 0) throw DeviceError("no CUDA device available (the B200 data plane has no CPU fallback)");
+  if (device < 0) SW_CUDA(cudaGetDevice(&device));
+  device_ = device;
+  SW_CUDA(cudaSetDevice(device_));
+  cudaStream_t s;
+  SW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  stream_ = s;
+  // Keep freed blocks in the pool: lists are re-allocated every level.
+  cudaMemPool_t pool;
+  SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
+  u64 thresh = ~u64{0};
+  SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+
+  // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
+  const InverseTransitions inv(aut);
+  std::vector<uint16_t> img(static_cast<size_t>(k_) * n_);
+  for (u32 a = 0; a < k_; ++a)
+    for (u32 q = 0; q < n_; ++q) img[static_cast<size_t>(a) * n_ + q] = static_cast<uint16_t>(aut.next(q, a));
+  std::vector<uint32_t> off(inv.offsets().begin(), inv.offsets().end());
+  std::vector<uint16_t> src(inv.sources_flat().begin(), inv.sources_flat().end());
+  void* p1 = alloc(img.size() * 2);
+  void* p2 = alloc(off.size() * 4);
+  void* p3 = alloc(src.size() * 2 + 2);
+  memcpy_h2d(p1, img.data(), img.size() * 2);
+  memcpy_h2d(p2, off.data(), off.size() * 4);
+  memcpy_h2d(p3, src.data(), src.size() * 2);
+  d_img = p1;
+  d_poff = p2;
+  d_psrc = p3;
+  sync();
+}
+
+Context::~Context() {
+  cudaSetDevice(device_);
+  for (auto& s : scratch_)
+    if (s.p) cudaFreeAsync(s.p, as_stream(stream_));
+  if (d_img) cudaFreeAsync(const_cast<void*>(d_img), as_stream(stream_));
+  if (d_poff) cudaFreeAsync(const_cast<void*>(d_poff), as_stream(stream_));
+  if (d_psrc) cudaFreeAsync(const_cast<void*>(d_psrc), as_stream(stream_));
+  cudaStreamSynchronize(as_stream(stream_));
+  cudaStreamDestroy(as_stream(stream_));
+}
+
+void* Context::alloc(size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  SW_CUDA(cudaMallocAsync(&p, bytes, as_stream(stream_)));
+  return p;
+}
+
+void Context::free(void* p) {
+  if (p) SW_CUDA(cudaFreeAsync(p, as_stream(stream_)));
+}
+
+void Context::sync() { SW_CUDA(cudaStreamSynchronize(as_stream(stream_))); }
+
+void Context::memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream_)));
+  sync();
+}
+
+void Context::memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream_)));
+}
+
+void* Context::scratch(int slot, size_t bytes) {
+  Scratch& s = scratch_[slot];
+  if (s.bytes < bytes) {
+    if (s.p) free(s.p);
+    s.bytes = bytes + bytes / 4 + 4096;
+    s.p = alloc(s.bytes);
+  }
+  return s.p;
+}
+
+// ------------------------------------------------------------------ DList
+DList::DList(Context* ctx, size_t cap, bool tagged) : ctx_(ctx), tagged_(tagged) { reserve(cap); }
+
+DList::~DList() { release(); }
+
+DList& DList::operator=(DList&& o) noexcept {
+  if (this != &o) {
+    release();
+    words = o.words;
+    cards = o.cards;
+    tags = o.tags;
+    ctx_ = o.ctx_;
+    size_ = o.size_;
+    cap_ = o.cap_;
+    tagged_ = o.tagged_;
+    o.words = nullptr;
+    o.cards = nullptr;
+    o.tags = nullptr;
+    o.size_ = o.cap_ = 0;
+  }
+  return *this;
+}
+
+void DList::release() {
+  if (ctx_) {
+    try {
+      ctx_->free(words);
+      ctx_->free(cards);
+      ctx_->free(tags);
+    } catch (...) {
+    }
+  }
+  words = nullptr;
+  cards = nullptr;
+  tags = nullptr;
+  size_ = cap_ = 0;
+}
+
+void DList::reserve(size_t cap) {
+  if (cap <= cap_ && words) return;
+  const size_t W = ctx_->W();
+  u64* nw = static_cast<u64*>(ctx_->alloc(cap * W * 8));
+  u32* nc = static_cast<u32*>(ctx_->alloc(cap * 4));
+  u64* nt = tagged_ ? static_cast<u64*>(ctx_->alloc(cap * 8)) : nullptr;
+  cudaStream_t s = as_stream(ctx_->stream());
+  if (size_) {
+    SW_CUDA(cudaMemcpyAsync(nw, words, size_ * W * 8, cudaMemcpyDeviceToDevice, s));
+    SW_CUDA(cudaMemcpyAsync(nc, cards, size_ * 4, cudaMemcpyDeviceToDevice, s));
+    if (tagged_) SW_CUDA(cudaMemcpyAsync(nt, tags, size_ * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  ctx_->free(words);
+  ctx_->free(cards);
+  ctx_->free(tags);
+  words = nw;
+  cards = nc;
+  tags = nt;
+  cap_ = cap;
+}
+
+void truncate(DList& l, size_t count) {
+  if (count < l.size()) l.set_size(count);
+}
+
+// ------------------------------------------------------------ transfers
+DList upload(Context& c, const u64* words, const u32* cards, const u64* tags, size_t count) {
+  DList l(&c, count, tags != nullptr);
+  c.memcpy_h2d(l.words, words, count * c.W() * 8);
+  if (cards) {
+    c.memcpy_h2d(l.cards, cards, count * 4);
+  } else {
+    std::vector<u32> cc(count);
+    for (size_t i = 0; i < count; ++i) {
+      u32 s = 0;
+      for (u32 w = 0; w < c.W(); ++w) s += static_cast<u32>(__builtin_popcountll(words[i * c.W() + w]));
+      cc[i] = s;
+    }
+    c.memcpy_h2d(l.cards, cc.data(), count * 4);
+    c.sync();
+  }
+  if (tags) c.memcpy_h2d(l.tags, tags, count * 8);
+  l.set_size(count);
+  c.sync();
+  return l;
+}
+
+void download(Context& c, const DList& l, u64* words, u32* cards, u64* tags) {
+  if (words) c.memcpy_d2h(words, l.words, l.size() * c.W() * 8);
+  if (cards) c.memcpy_d2h(cards, l.cards, l.size() * 4);
+  if (tags && l.tagged()) c.memcpy_d2h(tags, l.tags, l.size() * 8);
+}
+
+DList make_universe(Context& c, bool tagged) {
+  std::vector<u64> u = host_universe(c.n());
+  u32 card = c.n();
+  u64 tag = 0;
+  return upload(c, u.data(), &card, tagged ? &tag : nullptr, 1);
+}
+
+DList make_singletons(Context& c, bool tagged) {
+  const u32 n = c.n(), W = c.W();
+  std::vector<u64> w(static_cast<size_t>(n) * W, 0);
+  std::vector<u32> cards(n, 1);
+  std::vector<u64> tags(n);
+  for (u32 q = 0; q < n; ++q) {
+    w[static_cast<size_t>(q) * W + (q >> 6)] = state_bit(q);
+    tags[q] = q;
+  }
+  return upload(c, w.data(), cards.data(), tagged ? tags.data() : nullptr, n);
+}
+
+DList copy_list(Context& c, const DList& l, bool tagged) {
+  return slice_copy(c, l, 0, l.size(), tagged);
+}
+
+DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged) {
+  const size_t cnt = hi - lo;
+  DList out(&c, cnt, tagged && l.tagged());
+  cudaStream_t s = as_stream(c.stream());
+  if (cnt) {
+    SW_CUDA(cudaMemcpyAsync(out.words, l.words + lo * c.W(), cnt * c.W() * 8, cudaMemcpyDeviceToDevice, s));
+    SW_CUDA(cudaMemcpyAsync(out.cards, l.cards + lo, cnt * 4, cudaMemcpyDeviceToDevice, s));
+    if (out.tagged()) SW_CUDA(cudaMemcpyAsync(out.tags, l.tags + lo, cnt * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  out.set_size(cnt);
+  return out;
+}
+
+u64 read_tag(Context& c, const DList& l, size_t i) {
+  u64 t = 0;
+  if (!l.tagged()) throw std::logic_error("read_tag: untagged list");
+  c.memcpy_d2h(&t, l.tags + i, 8);
+  return t;
+}
+
+std::vector<u64> read_tags(Context& c, const DList& l) {
+  std::vector<u64> t(l.size());
+  if (l.tagged()) c.memcpy_d2h(t.data(), l.tags, l.size() * 8);
+  return t;
+}
+
+ContainIndex::~ContainIndex() {
+  if (ctx && nodes) {
+    try {
+      ctx->free(nodes);
+    } catch (...) {
+    }
+  }
+}
+ContainIndex::ContainIndex(ContainIndex&& o) noexcept { *this = std::move(o); }
+ContainIndex& ContainIndex::operator=(ContainIndex&& o) noexcept {
+  if (this != &o) {
+    if (ctx && nodes) ctx->free(nodes);
+    nodes = o.nodes;
+    count = o.count;
+    ctx = o.ctx;
+    o.nodes = nullptr;
+    o.count = 0;
+  }
+  return *this;
+}
+
+}  // namespace synchro::dev

@@ -1,0 +1,178 @@
+// Device data plane: HBM-resident set lists and the sm_100a kernels that
+// replace the reference's CPU set algebra.  Plain C++ interface (no CUDA
+// types leak out); implemented in device/*.cu.
+//
+// Layout in HBM: a list of N subsets of Q (|Q| = n) is SoA —
+//   words[N][W] u64, W = ceil(n/64), MSB-first packing (state 0 = bit 63 of
+//   word 0) so unsigned word order == the reference's lex order
+//   (state_set.hpp:14-19, set_list.hpp:34-38);
+//   cards[N] u32 (cached popcount);
+//   tags[N]  u64 (optional) = (parent_index << 16) | letter (bibfs_engine.hpp:362).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "../automaton.hpp"
+#include "../common.hpp"
+
+namespace synchro::dev {
+
+class Context;
+
+// Owning device list.  Move-only; memory is stream-ordered (cudaMallocAsync)
+// on the owning context's stream.
+class DList {
+ public:
+  DList() = default;
+  DList(Context* ctx, size_t cap, bool tagged);
+  ~DList();
+  DList(DList&& o) noexcept { *this = std::move(o); }
+  DList& operator=(DList&& o) noexcept;
+  DList(const DList&) = delete;
+  DList& operator=(const DList&) = delete;
+
+  void reserve(size_t cap);  // keeps contents
+  void release();
+  size_t size() const { return size_; }
+  bool empty() const { return size_ == 0; }
+  bool tagged() const { return tagged_; }
+  void set_size(size_t s) { size_ = s; }
+
+  u64* words = nullptr;
+  u32* cards = nullptr;
+  u64* tags = nullptr;
+
+ private:
+  Context* ctx_ = nullptr;
+  size_t size_ = 0;
+  size_t cap_ = 0;
+  bool tagged_ = false;
+  friend class Context;
+};
+
+struct ListStats {
+  u64 sum_cards = 0;
+  u32 min_card = 0;  // n for an empty list (set_list.hpp:182-186)
+  u32 max_card = 0;
+};
+
+struct Witness {
+  size_t a_index = 0;  // position in the A (subset-side) list
+  size_t b_index = 0;  // position in the B (superset-side) list
+};
+
+// Patricia/radix tree over a lex-sorted unique list (Karras 2012 layout:
+// N-1 internal nodes, node i covers a key range, splits at the first bit
+// where its keys differ) + per-node minimum cardinality.  Answers "is some
+// stored X a subset of query Y" with per-query traversal on the GPU.
+class ContainIndex {
+ public:
+  ContainIndex() = default;
+  ~ContainIndex();
+  ContainIndex(ContainIndex&&) noexcept;
+  ContainIndex& operator=(ContainIndex&&) noexcept;
+  void* nodes = nullptr;  // device Node[N-1]
+  size_t count = 0;       // keys indexed
+  Context* ctx = nullptr;
+};
+
+struct Counters {
+  u64 kernel_launches = 0;
+  u64 expand_launches = 0;
+  double expand_ms = 0;      // accumulated CUDA-event time of expansion kernels
+  u64 expand_children = 0;   // children produced by those launches
+  u64 contain_pair_tests = 0;
+};
+
+class Context {
+ public:
+  Context(const Automaton& aut, int device = -1);
+  ~Context();
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  u32 n() const { return n_; }
+  u32 k() const { return k_; }
+  u32 W() const { return W_; }
+  void* stream() const { return stream_; }
+  int device() const { return device_; }
+
+  void* alloc(size_t bytes);
+  void free(void* p);
+  void sync();
+  void memcpy_d2h(void* dst, const void* src, size_t bytes);
+  void memcpy_h2d(void* dst, const void* src, size_t bytes);
+
+  // Transition tables in device memory (uploaded once).
+  const void* d_img = nullptr;   // u16[k*n]  delta(q,a) at [a*n+q]
+  const void* d_poff = nullptr;  // u16/u32[k*n+1] CSR offsets of the inverse
+  const void* d_psrc = nullptr;  // u16[n*k] CSR sources
+  bool timing = false;           // record CUDA-event time of expansion kernels
+  Counters counters;
+
+  // Scratch buffers reused across calls (grown on demand).
+  void* scratch(int slot, size_t bytes);
+
+ private:
+  u32 n_, k_, W_;
+  int device_ = 0;
+  void* stream_ = nullptr;
+  struct Scratch { void* p = nullptr; size_t bytes = 0; };
+  Scratch scratch_[8];
+};
+
+// ---- list construction / transfer
+DList upload(Context& c, const u64* words, const u32* cards, const u64* tags, size_t count);
+void download(Context& c, const DList& l, u64* words, u32* cards, u64* tags);
+DList make_universe(Context& c, bool tagged);          // [Q], tag 0
+DList make_singletons(Context& c, bool tagged);        // {q} tagged q, q = 0..n-1
+DList copy_list(Context& c, const DList& l, bool tagged);
+
+// ---- expansion (replaces TransitionKernel::image/preimage + compute_layer,
+// bibfs_engine.hpp:345-367 and dfs_phase.hpp:93-103): children o = (i-lo)*k+a
+// of parents i in [lo,hi), card by popcount, tag (i<<16)|a when out is tagged.
+void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DList& out);
+
+void complement(Context& c, DList& l);                 // set_list.hpp:142-151
+ListStats stats(Context& c, const DList& l);
+
+// ---- ordering and deduplication (set_list.hpp:210-265)
+void sort_lex(Context& c, DList& l);                   // stable, index tie-break
+void sort_card_desc_lex(Context& c, DList& l);         // card desc, lex, index
+size_t dedupe_sorted(Context& c, DList& l);            // returns #removed
+size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
+
+// ---- containment (subset_algebra.hpp:138-231, static_trie.hpp:51-55)
+ContainIndex build_index(Context& c, const DList& a);  // a lex-sorted unique
+// Removes every b element that is a superset (proper: strict superset) of
+// some a element; b keeps its order.  Returns #removed.
+size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper);
+// keep[j] = 1 iff b[j] is not a (proper) superset of any a element.
+std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
+                                   bool proper);
+// Self-reduction to the minimal antichain (subset_algebra.hpp:179-197).
+size_t self_reduce_minimal(Context& c, DList& l);
+// Is some a element a subset of some b element?  (meet_check / trie query)
+bool exists_subset(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
+                   Witness* w);
+
+// ---- list surgery
+void keep_card_at_most(Context& c, DList& l, u32 max_card);
+void keep_card_at_least(Context& c, DList& l, u32 min_card);  // plain card of complements
+void truncate(DList& l, size_t count);
+DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged);
+// h := sorted merge of disjoint lex-sorted unique lists h and add (untagged).
+void merge_sorted(Context& c, DList& h, const DList& add);
+u64 read_tag(Context& c, const DList& l, size_t i);
+std::vector<u64> read_tags(Context& c, const DList& l);
+
+// ---- static trie shape (static_trie.hpp:85-151) for exact ledger accounting
+u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);
+
+// Device count / properties.
+int device_count();
+
+}  // namespace synchro::dev

@@ -1,0 +1,358 @@
+// Streaming kernels of the data plane: subset expansion (image / preimage),
+// complement, list statistics and order-preserving warp-ballot compaction.
+#include <cub/cub.cuh>
+
+#include "dev.hpp"
+#include "kernels.cuh"
+#include "util.cuh"
+
+namespace synchro::dev {
+
+// ---------------------------------------------------------------- expansion
+// One thread per parent set; the parent is read once and all k children are
+// produced from it (the reference's compute_layer i×a loop,
+// bibfs_engine.hpp:350-364, fused over letters).  Work is proportional to
+// |S| (scatter over set bits), not to n: image sets bit delta(q,a) for each
+// q in S; preimage sets the CSR row delta^-1(q,a) (mean in-degree 1).  The
+// tables (<= 24 KB) are staged in shared memory.
+template <int W, bool INV>
+__global__ void __launch_bounds__(256) expand_kernel(
+    const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
+    const uint16_t* __restrict__ g_img, const u32* __restrict__ g_off,
+    const uint16_t* __restrict__ g_src, u64* __restrict__ out, u32* __restrict__ out_card,
+    u64* __restrict__ out_tag) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const u32 kn = k * n;
+  u32* s_off = reinterpret_cast<u32*>(smem);
+  uint16_t* s_tab = INV ? reinterpret_cast<uint16_t*>(s_off + kn + 1)
+                        : reinterpret_cast<uint16_t*>(smem);
+  if (INV) {
+    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_src[i];
+  } else {
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
+  }
+  __syncthreads();
+
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    u64 s[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) s[w] = __ldg(src + (lo + i) * W + w);
+    for (u32 a = 0; a < k; ++a) {
+      u64 acc[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = 0;
+      const u32 base = a * n;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        u64 bits = s[w];
+        while (bits) {
+          const int b = __clzll(bits);
+          bits &= ~(u64{1} << (63 - b));
+          const u32 q = static_cast<u32>(w * 64 + b);
+          if (!INV) {
+            const u32 t = s_tab[base + q];
+            const u64 m = u64{1} << (63 - (t & 63));
+            const u32 tw = t >> 6;
+#pragma unroll
+            for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == tw) ? m : 0;
+          } else {
+            const u32 e1 = s_off[base + q + 1];
+            for (u32 e = s_off[base + q]; e < e1; ++e) {
+              const u32 t = s_tab[e];
+              const u64 m = u64{1} << (63 - (t & 63));
+              const u32 tw = t >> 6;
+#pragma unroll
+              for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == tw) ? m : 0;
+            }
+          }
+        }
+      }
+      const u64 o = i * k + a;
+      u32 c = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        out[o * W + w] = acc[w];
+        c += __popcll(acc[w]);
+      }
+      out_card[o] = c;
+      if (out_tag) out_tag[o] = ((lo + i) << 16) | a;
+    }
+  }
+}
+
+void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DList& out) {
+  const size_t cnt = hi > lo ? hi - lo : 0;
+  const u32 k = c.k(), n = c.n();
+  out.reserve(cnt * k);
+  out.set_size(cnt * k);
+  if (!cnt) return;
+  const size_t kn = static_cast<size_t>(k) * n;
+  const size_t shmem = inverse ? (kn + 1) * 4 + kn * 2 : kn * 2;
+  cudaStream_t s = as_stream(c.stream());
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c.timing) {
+    SW_CUDA(cudaEventCreate(&e0));
+    SW_CUDA(cudaEventCreate(&e1));
+    SW_CUDA(cudaEventRecord(e0, s));
+  }
+  const int block = 256;
+  const int grid = grid_for(cnt, block, 148 * 8);
+  SW_DISPATCH_W(c.W(), {
+    auto kern = inverse ? expand_kernel<W, true> : expand_kernel<W, false>;
+    if (shmem > 48 * 1024)
+      SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(shmem)));
+    kern<<<grid, block, shmem, s>>>(src.words, lo, cnt, n, k,
+                                    static_cast<const uint16_t*>(c.d_img),
+                                    static_cast<const u32*>(c.d_poff),
+                                    static_cast<const uint16_t*>(c.d_psrc), out.words, out.cards,
+                                    out.tagged() ? out.tags : nullptr);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+  c.counters.expand_launches++;
+  c.counters.expand_children += cnt * k;
+  if (c.timing) {
+    SW_CUDA(cudaEventRecord(e1, s));
+    SW_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SW_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    c.counters.expand_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+}
+
+// --------------------------------------------------------------- complement
+template <int W>
+__global__ void complement_kernel(u64* words, u32* cards, u64 count, u32 n) {
+  const u64 tail = (n & 63) ? (~u64{0} << (64 - (n & 63))) : ~u64{0};
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      u64 x = ~words[i * W + w];
+      if (w == W - 1) x &= tail;
+      words[i * W + w] = x;
+    }
+    cards[i] = n - cards[i];
+  }
+}
+
+void complement(Context& c, DList& l) {
+  if (l.empty()) return;
+  SW_DISPATCH_W(c.W(), {
+    complement_kernel<W><<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(
+        l.words, l.cards, l.size(), c.n());
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+}
+
+// -------------------------------------------------------------------- stats
+struct StatsAcc {
+  unsigned long long sum;
+  unsigned int min;
+  unsigned int max;
+};
+
+__global__ void stats_kernel(const u32* cards, u64 count, StatsAcc* acc) {
+  u64 sum = 0;
+  u32 mn = 0xFFFFFFFFu, mx = 0;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 v = cards[i];
+    sum += v;
+    mn = min(mn, v);
+    mx = max(mx, v);
+  }
+  using BR = cub::BlockReduce<u64, 256>;
+  using BR32 = cub::BlockReduce<u32, 256>;
+  __shared__ typename BR::TempStorage t1;
+  __shared__ typename BR32::TempStorage t2;
+  const u64 bs = BR(t1).Sum(sum);
+  __syncthreads();
+  const u32 bmn = BR32(t2).Reduce(mn, cub::Min());
+  __syncthreads();
+  const u32 bmx = BR32(t2).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) {
+    atomicAdd(&acc->sum, static_cast<unsigned long long>(bs));
+    atomicMin(&acc->min, bmn);
+    atomicMax(&acc->max, bmx);
+  }
+}
+
+ListStats stats(Context& c, const DList& l) {
+  ListStats st;
+  st.min_card = c.n();
+  if (l.empty()) return st;
+  StatsAcc h{0, 0xFFFFFFFFu, 0};
+  auto* d = static_cast<StatsAcc*>(c.scratch(7, sizeof(StatsAcc)));
+  c.memcpy_h2d(d, &h, sizeof(h));
+  stats_kernel<<<grid_for(l.size(), 256, 148 * 4), 256, 0, as_stream(c.stream())>>>(l.cards, l.size(), d);
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+  c.memcpy_d2h(&h, d, sizeof(h));
+  st.sum_cards = h.sum;
+  st.min_card = h.min;
+  st.max_card = h.max;
+  return st;
+}
+
+// --------------------------------------------------------------- compaction
+// Order-preserving stream compaction in two passes over tiles of 256 items:
+// (1) per-tile survivor counts from warp ballots, (2) a single-block scan of
+// the tile counts, (3) scatter: each survivor's slot = tile offset + warp
+// offset + popc(ballot & lanes_below).  Rows are optionally gathered through
+// a permutation (sorted order), so sort-apply + dedupe + compaction is one pass.
+constexpr int kTile = 256;
+
+template <class Keep>
+__global__ void __launch_bounds__(kTile) compact_count_kernel(u64 count, Keep keep, u32* tile_counts) {
+  const u64 i = static_cast<u64>(blockIdx.x) * kTile + threadIdx.x;
+  const bool f = i < count && keep(i);
+  const unsigned ballot = __ballot_sync(0xFFFFFFFFu, f);
+  __shared__ u32 warp_counts[kTile / 32];
+  if ((threadIdx.x & 31) == 0) warp_counts[threadIdx.x >> 5] = __popc(ballot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 s = 0;
+    for (int w = 0; w < kTile / 32; ++w) s += warp_counts[w];
+    tile_counts[blockIdx.x] = s;
+  }
+}
+
+// Exclusive scan of tile counts in one block; total written to tile_counts[ntiles].
+__global__ void __launch_bounds__(1024) scan_tiles_kernel(u32* tile_counts, u32 ntiles) {
+  using BS = cub::BlockScan<u32, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ u32 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u32 base = 0; base < ntiles; base += 1024) {
+    const u32 i = base + threadIdx.x;
+    const u32 v = i < ntiles ? tile_counts[i] : 0;
+    u32 ex, total;
+    BS(tmp).ExclusiveSum(v, ex, total);
+    if (i < ntiles) tile_counts[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_counts[ntiles] = carry;
+}
+
+template <int W, class Keep>
+__global__ void __launch_bounds__(kTile) compact_scatter_kernel(
+    u64 count, Keep keep, const u32* __restrict__ perm, const u32* __restrict__ tile_offsets,
+    const u64* __restrict__ sw, const u32* __restrict__ sc, const u64* __restrict__ st,
+    u64* __restrict__ dw, u32* __restrict__ dc, u64* __restrict__ dt) {
+  const u64 i = static_cast<u64>(blockIdx.x) * kTile + threadIdx.x;
+  const bool f = i < count && keep(i);
+  const unsigned ballot = __ballot_sync(0xFFFFFFFFu, f);
+  __shared__ u32 warp_off[kTile / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) warp_off[warp] = __popc(ballot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 s = 0;
+    for (int w = 0; w < kTile / 32; ++w) {
+      const u32 v = warp_off[w];
+      warp_off[w] = s;
+      s += v;
+    }
+  }
+  __syncthreads();
+  if (!f) return;
+  const u64 pos = tile_offsets[blockIdx.x] + warp_off[warp] + __popc(ballot & ((1u << lane) - 1));
+  const u64 from = perm ? perm[i] : i;
+#pragma unroll
+  for (int w = 0; w < W; ++w) dw[pos * W + w] = sw[from * W + w];
+  dc[pos] = sc[from];
+  if (dt) dt[pos] = st[from];
+}
+
+struct KeepAll {
+  __device__ bool operator()(u64) const { return true; }
+};
+struct KeepFlags {
+  const uint8_t* f;
+  __device__ bool operator()(u64 i) const { return f[i] != 0; }
+};
+template <int W>
+struct KeepUniqueSorted {  // first of each run of equal rows in perm order
+  const u64* words;
+  const u32* perm;
+  __device__ bool operator()(u64 i) const {
+    if (i == 0) return true;
+    const u64 a = perm ? perm[i] : i, b = perm ? perm[i - 1] : i - 1;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (words[a * W + w] != words[b * W + w]) return true;
+    return false;
+  }
+};
+
+template <int W, class Keep>
+static size_t run_compact(Context& c, DList& l, Keep keep, const u32* perm) {
+  const u64 count = l.size();
+  if (count == 0) return 0;
+  const u32 ntiles = static_cast<u32>((count + kTile - 1) / kTile);
+  auto* tiles = static_cast<u32*>(c.scratch(6, (ntiles + 1) * sizeof(u32)));
+  cudaStream_t s = as_stream(c.stream());
+  compact_count_kernel<<<ntiles, kTile, 0, s>>>(count, keep, tiles);
+  scan_tiles_kernel<<<1, 1024, 0, s>>>(tiles, ntiles);
+  u32 total = 0;
+  c.memcpy_d2h(&total, tiles + ntiles, 4);
+  DList out(&c, total, l.tagged());
+  if (total)
+    compact_scatter_kernel<W><<<ntiles, kTile, 0, s>>>(count, keep, perm, tiles, l.words, l.cards,
+                                                       l.tags, out.words, out.cards,
+                                                       l.tagged() ? out.tags : nullptr);
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 3;
+  out.set_size(total);
+  l = std::move(out);
+  return total;
+}
+
+size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm) {
+  size_t r = 0;
+  SW_DISPATCH_W(c.W(), {
+    if (keep)
+      r = run_compact<W>(c, l, KeepFlags{keep}, perm);
+    else
+      r = run_compact<W>(c, l, KeepAll{}, perm);
+  });
+  return r;
+}
+
+size_t compact_unique(Context& c, DList& l, const u32* perm) {
+  size_t r = 0;
+  SW_DISPATCH_W(c.W(), { r = run_compact<W>(c, l, KeepUniqueSorted<W>{l.words, perm}, perm); });
+  return r;
+}
+
+// ------------------------------------------------------ cardinality filters
+__global__ void card_filter_kernel(const u32* cards, u64 count, u32 bound, int at_least,
+                                   uint8_t* keep) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    keep[i] = at_least ? (cards[i] >= bound) : (cards[i] <= bound);
+}
+
+static void card_filter(Context& c, DList& l, u32 bound, int at_least) {
+  if (l.empty()) return;
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
+  card_filter_kernel<<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(
+      l.cards, l.size(), bound, at_least, keep);
+  SW_CHECK_LAUNCH();
+  compact_flags(c, l, keep, nullptr);
+}
+
+void keep_card_at_most(Context& c, DList& l, u32 max_card) { card_filter(c, l, max_card, 0); }
+void keep_card_at_least(Context& c, DList& l, u32 min_card) { card_filter(c, l, min_card, 1); }
+
+}  // namespace synchro::dev

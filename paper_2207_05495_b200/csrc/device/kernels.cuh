@@ -1,0 +1,24 @@
+// Internal cross-file entry points of the device layer.
+//
+// Scratch-slot convention (Context::scratch): 0/1 sort keys, 2/3 sort
+// permutations, 4 CUB temp storage, 5 flag arrays, 6 compaction tile counts,
+// 7 small reductions / result words.
+#pragma once
+
+#include <cstdint>
+
+#include "dev.hpp"
+
+namespace synchro::dev {
+
+// Keep rows with keep[i] != 0 (all rows when keep == nullptr), in order;
+// row i is read from position perm[i] when perm != nullptr.  Replaces l.
+size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm);
+// Keep the first row of every run of equal rows in perm order (sorted input).
+size_t compact_unique(Context& c, DList& l, const u32* perm);
+
+// Stable permutation sorting l lexicographically (optionally by descending
+// cardinality first); returned pointer lives in scratch slot 2 or 3.
+const u32* sort_perm(Context& c, const DList& l, bool card_desc);
+
+}  // namespace synchro::dev

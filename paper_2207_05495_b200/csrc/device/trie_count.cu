@@ -1,0 +1,236 @@
+// Exact node count of the reference's StaticTrie over a list, on the GPU.
+//
+// Only the NUMBER of trie nodes is observable in the reference (through the
+// ledger: footprint = sets + 24 B per node, static_trie.hpp:43-45, which
+// feeds peak_memory and the DFS slice cap).  The shape is a function of the
+// set family alone: build_node (static_trie.hpp:85-122) splits a range on the
+// state contained in the most (but not all) of its sets, ties to the smallest
+// state (pick_division_state, :127-151); ranges of <= min_leaf sets are
+// leaves; a zero side of <= min_leaf sets is absorbed as payload.
+//
+// Level-synchronous construction: every round processes all active segments
+// at once — (1) per-segment state histograms (shared-memory aggregation when a
+// block's elements fall into one segment, global atomics otherwise), (2) one
+// warp per segment picks the division state, (3) children are allocated and
+// counted, (4) elements are scattered to their child range (order inside a
+// range is irrelevant to the count).  Rounds = trie depth.
+#include <cub/cub.cuh>
+
+#include "dev.hpp"
+#include "kernels.cuh"
+#include "util.cuh"
+
+namespace synchro::dev {
+
+namespace {
+
+constexpr u32 kInvalid = 0xFFFFFFFFu;
+
+struct Seg {
+  u32 lo, hi;
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) hist_kernel(const u64* __restrict__ words,
+                                                   const u32* __restrict__ idx,
+                                                   const u32* __restrict__ seg, u32 N, u32 n,
+                                                   u32* __restrict__ hist) {
+  extern __shared__ u32 sh[];
+  const u32 base = blockIdx.x * blockDim.x;
+  const u32 i = base + threadIdx.x;
+  const u32 last = min(N, base + blockDim.x) - 1;
+  const u32 s0 = seg[base], s1 = seg[last];
+  const bool shared_mode = (s0 == s1) && s0 != kInvalid;
+  if (shared_mode) {
+    for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
+    __syncthreads();
+  }
+  if (i < N) {
+    const u32 s = seg[i];
+    if (s != kInvalid) {
+      const u64* x = words + static_cast<u64>(idx[i]) * W;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        u64 bits = x[w];
+        while (bits) {
+          const int b = __clzll(bits);
+          bits &= ~(u64{1} << (63 - b));
+          const u32 q = w * 64 + b;
+          if (shared_mode)
+            atomicAdd(&sh[q], 1u);
+          else
+            atomicAdd(&hist[static_cast<u64>(s) * n + q], 1u);
+        }
+      }
+    }
+  }
+  if (shared_mode) {
+    __syncthreads();
+    for (u32 q = threadIdx.x; q < n; q += blockDim.x)
+      if (sh[q]) atomicAdd(&hist[static_cast<u64>(s0) * n + q], sh[q]);
+  }
+}
+
+// One warp per active segment: division state, zero-side size, children.
+__global__ void pick_kernel(const u32* __restrict__ hist, const Seg* __restrict__ segs, u32 nseg,
+                            u32 n, u32 min_leaf, u32* __restrict__ div, u32* __restrict__ zcount,
+                            u32* __restrict__ child_zero, u32* __restrict__ child_one,
+                            Seg* __restrict__ next_segs, u32* __restrict__ next_count,
+                            unsigned long long* __restrict__ nodes) {
+  const u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nseg) return;
+  const Seg sg = segs[warp];
+  const u32 total = sg.hi - sg.lo;
+  const u32* h = hist + static_cast<u64>(warp) * n;
+  u32 best_c = 0, best_q = kInvalid;
+  for (u32 q = lane; q < n; q += 32) {
+    const u32 v = h[q];
+    if (v < total && v > best_c) {  // ascending q per lane: strict > keeps the smallest
+      best_c = v;
+      best_q = q;
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    const u32 oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, off);
+    const u32 oq = __shfl_xor_sync(0xFFFFFFFFu, best_q, off);
+    if (oc > best_c || (oc == best_c && oq < best_q)) {
+      best_c = oc;
+      best_q = oq;
+    }
+  }
+  if (lane == 0) {
+    // best_q == kInvalid only for duplicate sets (never for a deduped list).
+    div[warp] = best_q;
+    const u32 ones = best_c, zeros = total - ones;
+    zcount[warp] = zeros;
+    unsigned long long made = 1;  // the one side is always a node
+    u32 cz = kInvalid, co = kInvalid;
+    if (zeros > min_leaf) {
+      ++made;
+      cz = atomicAdd(next_count, 1u);
+      next_segs[cz] = Seg{sg.lo, sg.lo + zeros};
+    }
+    if (ones > min_leaf) {
+      co = atomicAdd(next_count, 1u);
+      next_segs[co] = Seg{sg.lo + zeros, sg.hi};
+    }
+    child_zero[warp] = cz;
+    child_one[warp] = co;
+    atomicAdd(nodes, made);
+  }
+}
+
+template <int W>
+__global__ void scatter_kernel(const u64* __restrict__ words, const u32* __restrict__ idx,
+                               const u32* __restrict__ seg, u32 N, const Seg* __restrict__ segs,
+                               const u32* __restrict__ div, const u32* __restrict__ zcount,
+                               const u32* __restrict__ child_zero, const u32* __restrict__ child_one,
+                               u32* __restrict__ cursor_zero, u32* __restrict__ cursor_one,
+                               u32* __restrict__ idx_out, u32* __restrict__ seg_out) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const u32 s = seg[i];
+  if (s == kInvalid) {
+    seg_out[i] = kInvalid;
+    idx_out[i] = idx[i];
+    return;
+  }
+  const u32 x = div[s];
+  const u32 e = idx[i];
+  const bool one = (words[static_cast<u64>(e) * W + (x >> 6)] >> (63 - (x & 63))) & 1;
+  u32 pos;
+  if (one)
+    pos = segs[s].lo + zcount[s] + atomicAdd(&cursor_one[s], 1u);
+  else
+    pos = segs[s].lo + atomicAdd(&cursor_zero[s], 1u);
+  idx_out[pos] = e;
+  seg_out[pos] = one ? child_one[s] : child_zero[s];
+}
+
+__global__ void init_kernel(u32* idx, u32* seg, u32 N) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) {
+    idx[i] = i;
+    seg[i] = 0;
+  }
+}
+
+}  // namespace
+
+u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
+  const u64 N64 = l.size();
+  if (N64 == 0) throw std::invalid_argument("StaticTrie: list must be non-empty");
+  min_leaf = std::max<u32>(1, min_leaf);
+  if (N64 <= min_leaf) return 1;
+  const u32 N = static_cast<u32>(N64), n = c.n();
+  cudaStream_t s = as_stream(c.stream());
+  u32* idx = static_cast<u32*>(c.alloc(N * 4ull));
+  u32* seg = static_cast<u32*>(c.alloc(N * 4ull));
+  u32* idx2 = static_cast<u32*>(c.alloc(N * 4ull));
+  u32* seg2 = static_cast<u32*>(c.alloc(N * 4ull));
+  init_kernel<<<(N + 255) / 256, 256, 0, s>>>(idx, seg, N);
+  const u32 max_segs = N / (min_leaf + 1) + 2;
+  Seg* segs = static_cast<Seg*>(c.alloc(max_segs * sizeof(Seg)));
+  Seg* nsegs = static_cast<Seg*>(c.alloc(max_segs * sizeof(Seg)));
+  // per-segment: div, zcount, child_zero, child_one, cursor_zero, cursor_one
+  u32* per = static_cast<u32*>(c.alloc(6ull * max_segs * 4));
+  struct Ctr {
+    u32 next_count;
+    u32 pad;
+    unsigned long long nodes;
+  };
+  Ctr* ctr = static_cast<Ctr*>(c.alloc(sizeof(Ctr)));
+  Ctr h{0, 0, 1};  // the root
+  c.memcpy_h2d(ctr, &h, sizeof(h));
+  Seg root{0, N};
+  c.memcpy_h2d(segs, &root, sizeof(root));
+  u32 nact = 1;
+  u32* hist = nullptr;
+  size_t hist_cap = 0;
+  while (nact > 0) {
+    const size_t hbytes = static_cast<size_t>(nact) * n * 4;
+    if (hbytes > hist_cap) {
+      if (hist) c.free(hist);
+      hist_cap = hbytes + hbytes / 2;
+      hist = static_cast<u32*>(c.alloc(hist_cap));
+    }
+    SW_CUDA(cudaMemsetAsync(hist, 0, hbytes, s));
+    SW_CUDA(cudaMemsetAsync(per, 0, 6ull * max_segs * 4, s));
+    SW_CUDA(cudaMemsetAsync(&ctr->next_count, 0, 4, s));
+    u32* div = per;
+    u32* zc = per + max_segs;
+    u32* cz = per + 2ull * max_segs;
+    u32* co = per + 3ull * max_segs;
+    u32* curz = per + 4ull * max_segs;
+    u32* curo = per + 5ull * max_segs;
+    SW_DISPATCH_W(c.W(), {
+      hist_kernel<W><<<(N + 255) / 256, 256, n * 4, s>>>(l.words, idx, seg, N, n, hist);
+    });
+    pick_kernel<<<(nact * 32 + 255) / 256, 256, 0, s>>>(hist, segs, nact, n, min_leaf, div, zc, cz,
+                                                        co, nsegs, &ctr->next_count, &ctr->nodes);
+    SW_DISPATCH_W(c.W(), {
+      scatter_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(l.words, idx, seg, N, segs, div, zc, cz, co,
+                                                        curz, curo, idx2, seg2);
+    });
+    SW_CHECK_LAUNCH();
+    c.counters.kernel_launches += 3;
+    std::swap(idx, idx2);
+    std::swap(seg, seg2);
+    std::swap(segs, nsegs);
+    c.memcpy_d2h(&h, ctr, sizeof(h));
+    nact = h.next_count;
+  }
+  c.free(idx);
+  c.free(seg);
+  c.free(idx2);
+  c.free(seg2);
+  c.free(segs);
+  c.free(nsegs);
+  c.free(per);
+  c.free(ctr);
+  if (hist) c.free(hist);
+  return h.nodes;
+}
+
+}  // namespace synchro::dev

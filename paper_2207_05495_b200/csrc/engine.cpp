@@ -1,0 +1,595 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <sstream>
+
+#include "device/dev.hpp"
+
+namespace synchro {
+namespace detail {
+
+using dev::DList;
+
+// ------------------------------------------------------------------ setup
+// L_BFS = [Q], H_BFS = [Q], L_IBFS = singletons tagged q, H_IBFS stored as
+// complements of the singletons; all four charged (bibfs_engine.hpp:68-95).
+GpuBibfs::GpuBibfs(const Automaton& aut, u64 upper_bound, const SolveOptions& opt,
+                   dev::Context& ctx)
+    : aut_(aut),
+      opt_(opt),
+      ctx_(ctx),
+      ledger_(opt.memory),
+      deadline_(Deadline::from_limit(opt.time_limit)),
+      n_(aut.state_count()),
+      k_(aut.alphabet_size()),
+      R_(upper_bound) {
+  lbfs_ = std::make_unique<DList>(dev::make_universe(ctx_, opt_.track_word));
+  hbfs_ = std::make_unique<DList>(dev::make_universe(ctx_, false));
+  libfs_ = std::make_unique<DList>(dev::make_singletons(ctx_, opt_.track_word));
+  hibfs_c_ = std::make_unique<DList>(dev::make_singletons(ctx_, false));
+  dev::complement(ctx_, *hibfs_c_);
+  refresh(*lbfs_, lbfs_i_);
+  refresh(*hbfs_, hbfs_i_);
+  refresh(*libfs_, libfs_i_);
+  refresh(*hibfs_c_, hibfs_i_);
+  ledger_.charge_or_throw(list_footprint(n_, lbfs_i_.size) + list_footprint(n_, libfs_i_.size) +
+                          list_footprint(n_, hbfs_i_.size) + list_footprint(n_, hibfs_i_.size));
+  h_bfs_last_reduced_ = hbfs_i_.size;
+  h_ibfs_last_reduced_ = hibfs_i_.size;
+}
+
+GpuBibfs::~GpuBibfs() = default;
+
+size_t GpuBibfs::bfs_size() const { return lbfs_i_.size; }
+size_t GpuBibfs::ibfs_size() const { return libfs_i_.size; }
+
+void GpuBibfs::refresh(const DList& l, Info& info) {
+  const dev::ListStats st = dev::stats(ctx_, l);
+  info.size = l.size();
+  info.sum_cards = st.sum_cards;
+  info.min_card = st.min_card;
+  info.max_card = st.max_card;
+}
+
+// set_list.hpp:171-174
+double GpuBibfs::density(const Info& i) const {
+  if (i.size == 0 || n_ == 0) return 0.0;
+  return static_cast<double>(i.sum_cards) / (static_cast<double>(n_) * i.size);
+}
+
+// ------------------------------------------------------------- statistics
+// bibfs_engine.hpp:107-147: identical integers in, identical doubles out.
+SearchStats GpuBibfs::make_stats() const {
+  SearchStats s;
+  s.k = k_;
+  s.r = static_cast<double>(r_);
+  s.R = static_cast<double>(R_);
+  const u64 used = ledger_.used(), budget = ledger_.budget();
+  const auto fits = [&](u64 extra, u64 freed) {
+    const u64 base = used > freed ? used - freed : 0;
+    return extra <= budget && base <= budget - extra;
+  };
+  s.bfs.list_size = static_cast<double>(lbfs_i_.size);
+  s.bfs.list_density = density(lbfs_i_);
+  s.bfs.hist_size = static_cast<double>(hbfs_i_.size);
+  s.bfs.hist_density = density(hbfs_i_);
+  s.bfs.r_dupl = ratio_bfs_[0];
+  s.bfs.r_self = ratio_bfs_[1];
+  s.bfs.r_hist = ratio_bfs_[2];
+  s.bfs.hist_dropped = bfs_hist_dropped_;
+  const u64 next_bfs = list_footprint(n_, static_cast<u64>(lbfs_i_.size) * k_);
+  s.bfs.step_feasible = !failed_[0] && fits(next_bfs, 0);
+  s.bfs.nh_feasible =
+      !failed_[1] && fits(next_bfs, bfs_hist_dropped_ ? 0 : list_footprint(n_, hbfs_i_.size));
+
+  s.ibfs.list_size = static_cast<double>(libfs_i_.size);
+  s.ibfs.list_density = density(libfs_i_);
+  s.ibfs.hist_size = static_cast<double>(hibfs_i_.size);
+  s.ibfs.hist_density = hibfs_i_.size == 0 ? 0.0 : 1.0 - density(hibfs_i_);
+  s.ibfs.r_dupl = ratio_ibfs_[0];
+  s.ibfs.r_self = ratio_ibfs_[1];
+  s.ibfs.r_hist = ratio_ibfs_[2];
+  s.ibfs.hist_dropped = ibfs_hist_dropped_;
+  const u64 next_ibfs = list_footprint(n_, static_cast<u64>(libfs_i_.size) * k_);
+  s.ibfs.step_feasible = !failed_[2] && fits(next_ibfs, 0);
+  s.ibfs.nh_feasible =
+      !failed_[3] && fits(next_ibfs, ibfs_hist_dropped_ ? 0 : list_footprint(n_, hibfs_i_.size));
+  s.dfs_feasible = true;
+  return s;
+}
+
+// ---------------------------------------------------------- ledger pieces
+void GpuBibfs::charge_layer(size_t parents) {
+  const u64 bytes = list_footprint(n_, static_cast<u64>(parents) * k_);
+  ledger_.charge_or_throw(bytes);
+  charged_layer_ = bytes;
+}
+
+void GpuBibfs::shrink_charge(size_t now_size) {
+  const u64 now = list_footprint(n_, now_size);
+  if (now < charged_layer_) ledger_.release(charged_layer_ - now);
+  charged_layer_ = now;
+}
+
+// Disjoint sorted merge; charges the merged list before releasing the old
+// one (bibfs_engine.hpp:383-403).
+void GpuBibfs::merge_history(DList& h, Info& hi, const DList& add) {
+  if (add.empty()) return;
+  const u64 before = list_footprint(n_, hi.size);
+  ledger_.charge_or_throw(list_footprint(n_, hi.size + add.size()));
+  dev::merge_sorted(ctx_, h, add);
+  refresh(h, hi);
+  ledger_.release(before);
+}
+
+void GpuBibfs::drop_bfs_history() {
+  if (bfs_hist_dropped_) return;
+  ledger_.release(list_footprint(n_, hbfs_i_.size));
+  *hbfs_ = DList(&ctx_, 0, false);
+  hbfs_i_ = Info{};
+  bfs_hist_dropped_ = true;
+}
+
+void GpuBibfs::drop_ibfs_history() {
+  if (ibfs_hist_dropped_) return;
+  ledger_.release(list_footprint(n_, hibfs_i_.size));
+  *hibfs_c_ = DList(&ctx_, 0, false);
+  hibfs_i_ = Info{};
+  ibfs_hist_dropped_ = true;
+}
+
+const dev::ContainIndex& GpuBibfs::bfs_index() {
+  if (!lbfs_index_) lbfs_index_ = std::make_unique<dev::ContainIndex>(dev::build_index(ctx_, *lbfs_));
+  return *lbfs_index_;
+}
+
+namespace {
+// Releases the charged layer if a step aborts between expansion and commit
+// (bibfs_engine.hpp:334-343).
+struct Rollback {
+  MemoryLedger& ledger;
+  u64& charged;
+  bool armed = true;
+  ~Rollback() {
+    if (armed) {
+      ledger.release(charged);
+      charged = 0;
+    }
+  }
+};
+inline double ratio(size_t part, size_t whole) {
+  return whole ? static_cast<double>(part) / static_cast<double>(whole) : 0.0;
+}
+}  // namespace
+
+// ------------------------------------------------------------ list steps
+// Forward step (bibfs_engine.hpp:152-191): [prune H] → expand → sort+dedupe →
+// minimal antichain → [drop supersets of H] → commit [→ merge into H].
+void GpuBibfs::bfs_step(bool with_history) {
+  if (!with_history) drop_bfs_history();
+  if (with_history && static_cast<double>(hbfs_i_.size) >=
+                          opt_.tuning.history_growth * static_cast<double>(h_bfs_last_reduced_)) {
+    const u64 before = list_footprint(n_, hbfs_i_.size);
+    dev::keep_card_at_most(ctx_, *hbfs_, lbfs_i_.max_card);
+    dev::self_reduce_minimal(ctx_, *hbfs_);
+    refresh(*hbfs_, hbfs_i_);
+    h_bfs_last_reduced_ = hbfs_i_.size;
+    ledger_.release(before - list_footprint(n_, hbfs_i_.size));
+  }
+  charge_layer(lbfs_i_.size);
+  DList next(&ctx_, lbfs_i_.size * k_, opt_.track_word);
+  dev::expand(ctx_, *lbfs_, 0, lbfs_i_.size, /*inverse=*/false, next);
+  Rollback rb{ledger_, charged_layer_};
+  const size_t generated = next.size();
+  const double r_dupl = generated ? ratio(dev::lex_sort_dedupe(ctx_, next), generated) : 0.0;
+  const size_t after_dupl = next.size();
+  const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
+  double r_hist = 0.0;
+  if (with_history) {
+    const size_t before = next.size();
+    const dev::ContainIndex hix = dev::build_index(ctx_, *hbfs_);
+    const size_t removed = dev::remove_supersets(ctx_, *hbfs_, hix, next, /*proper=*/false);
+    r_hist = ratio(removed, before);
+  }
+  shrink_charge(next.size());
+  if (with_history) merge_history(*hbfs_, hbfs_i_, next);
+  // commit (bibfs_engine.hpp:375-379)
+  ledger_.release(list_footprint(n_, lbfs_i_.size));
+  *lbfs_ = std::move(next);
+  lbfs_index_.reset();
+  refresh(*lbfs_, lbfs_i_);
+  charged_layer_ = 0;
+  rb.armed = false;
+  if (opt_.track_word) bfs_levels_.push_back(dev::read_tags(ctx_, *lbfs_));
+  ratio_bfs_[0] = 0.5 * ratio_bfs_[0] + 0.5 * r_dupl;
+  ratio_bfs_[1] = 0.5 * ratio_bfs_[1] + 0.5 * r_self;
+  if (with_history) ratio_bfs_[2] = 0.5 * ratio_bfs_[2] + 0.5 * r_hist;
+}
+
+// Inverse step (bibfs_engine.hpp:195-238): all reductions on complements, so
+// the kept plain sets are the maximal ones; L_IBFS is committed in
+// complement-lex order, H_IBFS stays complemented.
+void GpuBibfs::ibfs_step(bool with_history) {
+  if (!with_history) drop_ibfs_history();
+  if (with_history && static_cast<double>(hibfs_i_.size) >=
+                          opt_.tuning.history_growth * static_cast<double>(h_ibfs_last_reduced_)) {
+    const u64 before = list_footprint(n_, hibfs_i_.size);
+    // keep complements whose plain cardinality n - c is >= min card of L_IBFS
+    dev::keep_card_at_most(ctx_, *hibfs_c_, n_ - libfs_i_.min_card);
+    dev::self_reduce_minimal(ctx_, *hibfs_c_);
+    refresh(*hibfs_c_, hibfs_i_);
+    h_ibfs_last_reduced_ = hibfs_i_.size;
+    ledger_.release(before - list_footprint(n_, hibfs_i_.size));
+  }
+  charge_layer(libfs_i_.size);
+  DList next(&ctx_, libfs_i_.size * k_, opt_.track_word);
+  dev::expand(ctx_, *libfs_, 0, libfs_i_.size, /*inverse=*/true, next);
+  Rollback rb{ledger_, charged_layer_};
+  dev::complement(ctx_, next);
+  const size_t generated = next.size();
+  const double r_dupl = generated ? ratio(dev::lex_sort_dedupe(ctx_, next), generated) : 0.0;
+  const size_t after_dupl = next.size();
+  const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
+  double r_hist = 0.0;
+  if (with_history) {
+    const size_t before = next.size();
+    const dev::ContainIndex hix = dev::build_index(ctx_, *hibfs_c_);
+    const size_t removed = dev::remove_supersets(ctx_, *hibfs_c_, hix, next, /*proper=*/false);
+    r_hist = ratio(removed, before);
+  }
+  shrink_charge(next.size());
+  if (with_history) merge_history(*hibfs_c_, hibfs_i_, next);
+  dev::complement(ctx_, next);
+  ledger_.release(list_footprint(n_, libfs_i_.size));
+  *libfs_ = std::move(next);
+  refresh(*libfs_, libfs_i_);
+  charged_layer_ = 0;
+  rb.armed = false;
+  if (opt_.track_word) ibfs_levels_.push_back(dev::read_tags(ctx_, *libfs_));
+  ratio_ibfs_[0] = 0.5 * ratio_ibfs_[0] + 0.5 * r_dupl;
+  ratio_ibfs_[1] = 0.5 * ratio_ibfs_[1] + 0.5 * r_self;
+  if (with_history) ratio_ibfs_[2] = 0.5 * ratio_ibfs_[2] + 0.5 * r_hist;
+}
+
+void GpuBibfs::perform(StepKind kind) {
+  switch (kind) {
+    case StepKind::BFS: return bfs_step(true);
+    case StepKind::BFS_NH: return bfs_step(false);
+    case StepKind::IBFS: return ibfs_step(true);
+    case StepKind::IBFS_NH: return ibfs_step(false);
+    case StepKind::DFS: break;
+  }
+  throw std::logic_error("perform: DFS is not a list step");
+}
+
+// Meet: is some X in L_BFS a subset of some Y in L_IBFS?
+bool GpuBibfs::meet() { return dev::exists_subset(ctx_, *lbfs_, bfs_index(), *libfs_, nullptr); }
+
+bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
+  dev::Witness w;
+  if (!dev::exists_subset(ctx_, *lbfs_, bfs_index(), *libfs_, &w)) return false;
+  *bfs_index_out = w.a_index;
+  *ibfs_tag = dev::read_tag(ctx_, *libfs_, w.b_index);
+  return true;
+}
+
+// -------------------------------------------------------------- DFS phase
+namespace {
+
+// Level-by-level inverse DFS below the frozen L_BFS (dfs_phase.hpp:47-177):
+// the recursion, slicing and ledger stay on the host; every level's
+// preimages, (card desc, lex) order, dedupe, window pruning and containment
+// query against L_BFS are device kernels.
+class DfsRunner {
+ public:
+  DfsRunner(dev::Context& c, const DList& lbfs, const dev::ContainIndex& index,
+            MemoryLedger& ledger, const EngineTuning& t, const Deadline& deadline, bool tracking,
+            std::vector<std::array<u64, 5>>* log)
+      : c_(c), lbfs_(lbfs), index_(index), ledger_(ledger), t_(t), deadline_(deadline),
+        tracking_(tracking), log_(log) {}
+
+  u64 run(const DList& initial, u64 r0, u64 bound) {
+    bound_ = bound;
+    if (r0 >= bound_ || initial.empty()) return bound_;
+    const size_t cap = slice_cap(r0 - 1);
+    for (size_t lo = 0; lo < initial.size(); lo += cap) {
+      recurse(initial, lo, std::min(initial.size(), lo + cap), r0, 0, nullptr);
+      if (r0 >= bound_) break;
+    }
+    return bound_;
+  }
+  const DfsFind& find() const { return find_; }
+  u64 expansions = 0;
+
+ private:
+  struct Frame {
+    const Frame* up;
+    const DList* list;
+  };
+  struct Guard {
+    MemoryLedger& l;
+    u64 amount;
+    ~Guard() { l.release(amount); }
+  };
+
+  size_t slice_cap(u64 r) const {
+    const u64 set_bytes = words_for(c_.n()) * sizeof(u64);
+    const u64 levels = bound_ > r ? bound_ - r : 1;
+    const u64 denom = (c_.k() + 1) * levels * set_bytes;
+    return static_cast<size_t>(std::max<u64>(ledger_.available() / std::max<u64>(denom, 1), 1));
+  }
+
+  void recurse(const DList& list, size_t lo, size_t hi, u64 r, u32 level, const Frame* parent) {
+    deadline_.check();
+    const u32 k = c_.k(), n = c_.n();
+    const u64 charged = list_footprint(n, static_cast<u64>(hi - lo) * k);
+    ledger_.charge_or_throw(charged);
+    Guard guard{ledger_, charged};
+    DList next(&c_, (hi - lo) * k, tracking_);
+    dev::expand(c_, list, lo, hi, /*inverse=*/true, next);
+    expansions += static_cast<u64>(hi - lo) * k;
+    const u64 generated = next.size();
+    dev::sort_card_desc_lex(c_, next);
+    if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0) dev::dedupe_sorted(c_, next);
+    if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
+      // Drop sets that are proper subsets of one of the dfs_largest first
+      // (largest) sets — proper-superset marking on complements.
+      DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
+      dev::complement(c_, largest);
+      dev::lex_sort_dedupe(c_, largest);
+      const dev::ContainIndex lix = dev::build_index(c_, largest);
+      dev::complement(c_, next);
+      dev::remove_supersets(c_, largest, lix, next, /*proper=*/true);
+      dev::complement(c_, next);
+    }
+    const u64 now = list_footprint(n, next.size());
+    if (now < charged) {
+      ledger_.release(charged - now);
+      guard.amount = now;
+    }
+    if (log_) log_->push_back({r, level, hi - lo, generated, next.size()});
+    dev::Witness w;
+    if (dev::exists_subset(c_, lbfs_, index_, next, tracking_ ? &w : nullptr)) {
+      bound_ = r;
+      if (tracking_) record_find(w, next, parent);
+      return;
+    }
+    if (r >= bound_ - 1) return;
+    const Frame frame{parent, &next};
+    const size_t cap = slice_cap(r);
+    for (size_t plo = 0; plo < next.size(); plo += cap) {
+      recurse(next, plo, std::min(next.size(), plo + cap), r + 1, level + 1, &frame);
+      if (r >= bound_ - 1) return;
+    }
+  }
+
+  void record_find(const dev::Witness& w, const DList& level, const Frame* parent) {
+    find_.found = true;
+    find_.trie_index = w.a_index;
+    find_.middle.clear();
+    u64 tag = dev::read_tag(c_, level, w.b_index);
+    for (const Frame* f = parent;; f = f->up) {
+      find_.middle.push_back(static_cast<u32>(tag & 0xFFFF));
+      const size_t idx = static_cast<size_t>(tag >> 16);
+      if (!f) {
+        find_.root_index = idx;
+        break;
+      }
+      tag = dev::read_tag(c_, *f->list, idx);
+    }
+  }
+
+  dev::Context& c_;
+  const DList& lbfs_;
+  const dev::ContainIndex& index_;
+  MemoryLedger& ledger_;
+  const EngineTuning& t_;
+  const Deadline& deadline_;
+  bool tracking_;
+  std::vector<std::array<u64, 5>>* log_;
+  u64 bound_ = 0;
+  DfsFind find_;
+};
+
+}  // namespace
+
+// bibfs_engine.hpp:275-298: drop histories, freeze L_BFS as the containment
+// structure (charged as the reference's trie: sets + 24 B per trie node),
+// run the DFS from L_IBFS.
+u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log,
+                      u64* expansions) {
+  drop_bfs_history();
+  drop_ibfs_history();
+  if (lbfs_i_.size == 0) return R_;
+  const u64 nodes = dev::trie_node_count(ctx_, *lbfs_, opt_.tuning.min_leaf);
+  const u64 trie_bytes = list_footprint(n_, lbfs_i_.size) + nodes * 24;
+  ledger_.charge_or_throw(trie_bytes);
+  ledger_.release(list_footprint(n_, lbfs_i_.size));
+  const dev::ContainIndex& index = bfs_index();
+  DfsRunner dfs(ctx_, *lbfs_, index, ledger_, opt_.tuning, deadline_, opt_.track_word, log);
+  const u64 final_bound = dfs.run(*libfs_, r, R_);
+  if (find) *find = dfs.find();
+  if (expansions) *expansions = dfs.expansions;
+  ledger_.release(trie_bytes);
+  R_ = final_bound;
+  return final_bound;
+}
+
+// ------------------------------------------------------- reconstruction
+Word GpuBibfs::bfs_prefix(size_t index) const {
+  Word w;
+  size_t idx = index;
+  for (size_t lvl = bfs_levels_.size(); lvl-- > 0;) {
+    const u64 tag = bfs_levels_[lvl][idx];
+    w.push_back(static_cast<u32>(tag & 0xFFFF));
+    idx = static_cast<size_t>(tag >> 16);
+  }
+  std::reverse(w.begin(), w.end());
+  return w;
+}
+
+Word GpuBibfs::ibfs_suffix_from_tag(u64 tag) const {
+  Word w;
+  for (size_t lvl = ibfs_levels_.size(); lvl-- > 0;) {
+    w.push_back(static_cast<u32>(tag & 0xFFFF));
+    if (lvl == 0) break;
+    tag = ibfs_levels_[lvl - 1][static_cast<size_t>(tag >> 16)];
+  }
+  return w;
+}
+
+Word GpuBibfs::ibfs_suffix_from_index(size_t index) const {
+  if (ibfs_levels_.empty()) return {};
+  return ibfs_suffix_from_tag(ibfs_levels_.back()[index]);
+}
+
+// bibfs_engine.hpp:442-460 (same keys, same default ostream formatting).
+void trace_line(std::ostream* trace, const GpuBibfs& eng, const SearchStats& s, const StepCosts& c,
+                StepKind kind) {
+  if (!trace) return;
+  std::ostringstream os;
+  os << "iter=" << eng.iteration() << " step=" << step_kind_name(kind)
+     << " lbfs=" << static_cast<u64>(s.bfs.list_size) << " libfs=" << static_cast<u64>(s.ibfs.list_size)
+     << " hbfs=" << static_cast<u64>(s.bfs.hist_size) << " hibfs=" << static_cast<u64>(s.ibfs.hist_size)
+     << " d_lbfs=" << s.bfs.list_density << " d_libfs=" << s.ibfs.list_density
+     << " rdupl_bfs=" << s.bfs.r_dupl << " rself_bfs=" << s.bfs.r_self << " rhist_bfs=" << s.bfs.r_hist
+     << " rdupl_ibfs=" << s.ibfs.r_dupl << " rself_ibfs=" << s.ibfs.r_self
+     << " rhist_ibfs=" << s.ibfs.r_hist << " cost_bfs=" << c.step[0] << " cost_bfs_nh=" << c.step[1]
+     << " cost_ibfs=" << c.step[2] << " cost_ibfs_nh=" << c.step[3] << " pred_bfs=" << c.pred[0]
+     << " pred_bfs_nh=" << c.pred[1] << " pred_ibfs=" << c.pred[2] << " pred_ibfs_nh=" << c.pred[3]
+     << " pred_dfs=" << c.pred[4];
+  *trace << os.str() << '\n';
+}
+
+}  // namespace detail
+
+// --------------------------------------------------------------- solve
+SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
+  if (!is_synchronizing(aut)) throw NotSynchronizingError();
+  SolveResult res;
+  if (aut.state_count() == 1) {
+    res.phase = "trivial";
+    if (opt.track_word) res.word = Word{};
+    return res;
+  }
+  dev::Context ctx(aut, opt.device);
+  ctx.timing = opt.timing;
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  std::optional<HeuristicResult> heur;
+  u64 R;
+  if (opt.upper_bound) {
+    R = *opt.upper_bound;
+  } else {
+    AdaptiveOptions aopt;
+    aopt.memory = opt.memory;
+    aopt.initial_beam = opt.tuning.beam_initial;
+    aopt.cost_fraction = opt.tuning.beam_cost_fraction;
+    aopt.set_cost = opt.tuning.cost.set_cost;
+    aopt.deadline = Deadline::from_limit(opt.time_limit);
+    heur = adaptive_upper_bound(aut, aopt, &ctx);
+    R = heur->length;
+  }
+  res.upper_bound = R;
+  const auto t1 = clock::now();
+  res.heuristic_seconds = std::chrono::duration<double>(t1 - t0).count();
+
+  detail::GpuBibfs eng(aut, R, opt, ctx);
+  const auto finish = [&](u64 threshold, std::optional<Word> word, const char* phase) {
+    res.threshold = threshold;
+    res.word = std::move(word);
+    res.peak_memory = eng.ledger().peak();
+    res.phase = phase;
+    res.engine_seconds = std::chrono::duration<double>(clock::now() - t1).count();
+    res.expand_kernel_ms = ctx.counters.expand_ms;
+    res.kernel_launches = ctx.counters.kernel_launches;
+    return res;
+  };
+
+  for (u64 r = 1; r + 1 <= R; ++r) {
+    eng.deadline().check();
+    eng.set_iteration(r);
+    eng.clear_failures();
+    ++res.iterations;
+    StepKind kind = StepKind::DFS;
+    SearchStats st;
+    StepCosts sc;
+    while (true) {
+      st = eng.make_stats();
+      sc = compute_step_costs(st, opt.tuning.cost);
+      switch (opt.schedule) {
+        case Schedule::Auto: kind = select_step(sc); break;
+        case Schedule::BfsOnly:
+          kind = sc.feasible[0] ? StepKind::BFS : (sc.feasible[1] ? StepKind::BFS_NH : StepKind::DFS);
+          break;
+        case Schedule::IbfsOnly:
+          kind = sc.feasible[2] ? StepKind::IBFS : (sc.feasible[3] ? StepKind::IBFS_NH : StepKind::DFS);
+          break;
+        case Schedule::DfsImmediate: kind = StepKind::DFS; break;
+      }
+      if (kind == StepKind::DFS) break;
+      const u64 parents = (kind == StepKind::BFS || kind == StepKind::BFS_NH) ? eng.bfs_size()
+                                                                              : eng.ibfs_size();
+      try {
+        eng.perform(kind);
+        res.expansions_phase1 += parents * aut.alphabet_size();
+        break;
+      } catch (const OutOfMemoryError&) {
+        eng.mark_failed(kind);  // engine rolled back; choose again
+      }
+    }
+
+    if (kind == StepKind::DFS) {
+      res.used_dfs = true;
+      if (opt.trace) *opt.trace << "iter=" << r << " step=DFS handoff\n";
+      DfsFind find;
+      const u64 threshold = eng.run_dfs(r, &find, &res.dfs_levels, &res.expansions_dfs);
+      if (opt.trace) *opt.trace << "result=" << threshold << " phase=dfs\n";
+      std::optional<Word> word;
+      if (opt.track_word) {
+        if (find.found) {
+          Word w = eng.bfs_prefix(find.trie_index);
+          w.insert(w.end(), find.middle.begin(), find.middle.end());
+          const Word tail = eng.ibfs_suffix_from_index(find.root_index);
+          w.insert(w.end(), tail.begin(), tail.end());
+          if (w.size() != threshold || !is_reset_word(aut, w))
+            throw std::logic_error("reconstructed word is not a valid witness");
+          word = std::move(w);
+        } else if (heur && heur->length == threshold) {
+          word = heur->word;
+        }
+      }
+      return finish(threshold, std::move(word), "dfs");
+    }
+
+    if (kind == StepKind::BFS || kind == StepKind::BFS_NH)
+      ++res.bfs_steps;
+    else
+      ++res.ibfs_steps;
+    detail::trace_line(opt.trace, eng, st, sc, kind);
+
+    if (opt.track_word) {
+      size_t bi = 0;
+      u64 tag = 0;
+      if (eng.meet_witness(&bi, &tag)) {
+        Word full = eng.bfs_prefix(bi);
+        const Word tail = eng.ibfs_suffix_from_tag(tag);
+        full.insert(full.end(), tail.begin(), tail.end());
+        if (full.size() != r || !is_reset_word(aut, full))
+          throw std::logic_error("reconstructed word is not a valid witness");
+        if (opt.trace) *opt.trace << "result=" << r << " phase=meet\n";
+        return finish(r, std::move(full), "meet");
+      }
+    } else if (eng.meet()) {
+      if (opt.trace) *opt.trace << "result=" << r << " phase=meet\n";
+      return finish(r, std::nullopt, "meet");
+    }
+  }
+  if (opt.trace) *opt.trace << "result=" << R << " phase=bound\n";
+  std::optional<Word> word;
+  if (opt.track_word && heur) word = heur->word;
+  return finish(R, std::move(word), "bound");
+}
+
+}  // namespace synchro

@@ -1,0 +1,105 @@
+"""Parity of each B200 data-plane primitive against the reference (oracle/_ref),
+called through the C-ABI (include/synchro_b200.h) on seeded random lists.
+
+Bar: bit-exact — same words, same order, same cardinalities, same surviving
+tags (which duplicate survives, set_list.hpp:208-209).
+"""
+import numpy as np
+import pytest
+
+from helpers import W, lex_sorted_unique, random_list, rows
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(20, 0.3), (64, 0.1), (100, 0.08), (300, 0.077), (570, 0.05), (129, 0.5), (1, 0.5)]
+
+
+@pytest.mark.parametrize("n,k,seed", [(20, 2, 0), (100, 2, 3), (300, 2, 0), (570, 2, 1),
+                                      (200, 3, 0), (26, 25, 4), (64, 2, 5), (1, 1, 0)])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_expand_matches_transition_kernel(gpu, ref, n, k, seed, inverse):
+    aut = gpu.random_automaton(n, k, seed)
+    words = random_list(n, 3000, 0.1, seed + 11)
+    ow, oc = gpu.list_expand(aut, words, inverse)
+    rw, rc = ref.expand(n, k, aut.delta, words, inverse)
+    assert np.array_equal(ow, rw)
+    assert np.array_equal(oc, rc)
+
+
+def test_expand_empty_list(gpu):
+    aut = gpu.random_automaton(50, 2, 1)
+    ow, oc = gpu.list_expand(aut, np.zeros(0, np.uint64), False)
+    assert ow.size == 0 and oc.size == 0
+
+
+@pytest.mark.parametrize("n,density", SHAPES)
+def test_lex_sort_dedupe(gpu, ref, n, density):
+    base = random_list(n, 1500, density, 7)
+    words = np.concatenate([base, base[: 600 * W(n)], random_list(n, 500, density, 8)])
+    tags = np.arange(words.size // W(n), dtype=np.uint64) * 7 + 3
+    gw, gc, gt = gpu.list_lex_sort_dedupe(n, words, tags)
+    rw, rc, rt, _ = ref.lex_sort_dedupe(n, words, tags)
+    assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
+
+
+@pytest.mark.parametrize("n,density", SHAPES)
+def test_sort_card_desc_lex_and_dedupe(gpu, ref, n, density):
+    base = random_list(n, 2000, density, 9)
+    words = np.concatenate([base, base[: 300 * W(n)]])
+    tags = np.arange(words.size // W(n), dtype=np.uint64)
+    gw, gc, gt = gpu.list_sort_card_desc_lex(n, words, tags)
+    rw, rc, rt = ref.sort_card_desc_lex(n, words, tags)
+    assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
+    dw, dc, dt = gpu.list_dedupe_sorted(n, gw, gt)
+    assert len(set(rows(n, dw))) == dw.size // W(n) == len(set(rows(n, words)))
+
+
+@pytest.mark.parametrize("n,density,count", [(20, 0.3, 3000), (100, 0.08, 20000),
+                                             (300, 0.077, 30000), (300, 0.95, 3000),
+                                             (570, 0.06, 20000), (64, 0.5, 4000), (2, 0.5, 4)])
+def test_self_reduce_minimal(gpu, ref, n, density, count):
+    words = lex_sorted_unique(n, random_list(n, count, density, count))
+    g = gpu.list_self_reduce_minimal(n, words)
+    r = ref.self_reduce_minimal(n, words)
+    assert np.array_equal(g, r)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("n,da,db", [(30, 0.2, 0.5), (100, 0.05, 0.3), (300, 0.05, 0.2),
+                                     (300, 0.9, 0.95), (570, 0.03, 0.2)])
+def test_mark_modes(gpu, ref, mode, n, da, db):
+    a = lex_sorted_unique(n, random_list(n, 4000, da, 1))
+    b = random_list(n, 6000, db, 2)
+    b = np.concatenate([b, a[: 100 * W(n)]])  # equal sets exercise proper vs non-proper
+    g = gpu.list_mark(n, a, b, mode)
+    r = ref.mark(n, a, b, mode)
+    assert np.array_equal(g, r)
+    assert 0 < int(g.sum()) < g.size or n == 570
+
+
+def test_mark_rejects_unsorted_a(gpu):
+    n = 40
+    a = random_list(n, 50, 0.3, 3)
+    b = random_list(n, 50, 0.3, 4)
+    with pytest.raises(gpu.SynchroError):
+        gpu.list_mark(n, a[::-1].copy(), b, 0)
+
+
+@pytest.mark.parametrize("n,da,db,seed", [(100, 0.1, 0.4, 0), (300, 0.08, 0.3, 1),
+                                          (300, 0.08, 0.1, 2), (64, 0.3, 0.3, 3)])
+def test_meet_check(gpu, ref, n, da, db, seed):
+    a = lex_sorted_unique(n, random_list(n, 20000, da, seed))
+    b = random_list(n, 2000, db, seed + 100)
+    assert gpu.list_meet_check(n, a, b) == ref.meet_check(n, a, b)
+    # planted containment
+    b2 = b.copy()
+    b2[: W(n)] = a[5 * W(n): 6 * W(n)] | b2[: W(n)]
+    assert gpu.list_meet_check(n, a, b2) and ref.meet_check(n, a, b2)
+
+
+@pytest.mark.parametrize("n,density,count,min_leaf", [(20, 0.3, 500, 10), (100, 0.08, 20000, 10),
+                                                      (300, 0.077, 50000, 10), (300, 0.95, 5000, 10),
+                                                      (570, 0.05, 30000, 3), (64, 0.5, 7, 10)])
+def test_trie_node_count(gpu, ref, n, density, count, min_leaf):
+    words = lex_sorted_unique(n, random_list(n, count, density, count + 1))
+    assert gpu.trie_node_count(n, words, min_leaf) == ref.trie_node_count(n, words, min_leaf)[0]
