@@ -89,6 +89,9 @@ typedef struct sw_solve_result {
   double expand_kernel_ms;
   uint64_t kernel_launches;
   char phase[16];           /* "meet" | "dfs" | "bound" | "trivial" */
+  double engine_device_ms;  /* CUDA-event span of the engine on its stream */
+  uint64_t h2d_bytes;       /* host->device bytes copied during the solve */
+  uint64_t d2h_bytes;       /* device->host bytes copied during the solve */
 } sw_solve_result;
 
 const char* sw_version(void);

@@ -199,6 +199,9 @@ SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
     out->engine_seconds = r.engine_seconds;
     out->expand_kernel_ms = r.expand_kernel_ms;
     out->kernel_launches = r.kernel_launches;
+    out->engine_device_ms = r.engine_device_ms;
+    out->h2d_bytes = r.h2d_bytes;
+    out->d2h_bytes = r.d2h_bytes;
     std::strncpy(out->phase, r.phase.c_str(), sizeof(out->phase) - 1);
     if (r.word && word)
       for (size_t i = 0; i < r.word->size() && i < word_cap; ++i) word[i] = (*r.word)[i];

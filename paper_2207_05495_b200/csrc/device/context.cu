@@ -88,14 +88,36 @@ void Context::free(void* p) {
 
 void Context::sync() { SW_CUDA(cudaStreamSynchronize(as_stream(stream_))); }
 
+StreamTimer::StreamTimer(Context& c) : c_(c) {
+  cudaEvent_t a, b;
+  SW_CUDA(cudaEventCreate(&a));
+  SW_CUDA(cudaEventCreate(&b));
+  e0_ = a;
+  e1_ = b;
+}
+StreamTimer::~StreamTimer() {
+  cudaEventDestroy(static_cast<cudaEvent_t>(e0_));
+  cudaEventDestroy(static_cast<cudaEvent_t>(e1_));
+}
+void StreamTimer::start() { SW_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(e0_), as_stream(c_.stream()))); }
+double StreamTimer::stop_ms() {
+  SW_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(e1_), as_stream(c_.stream())));
+  SW_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(e1_)));
+  float ms = 0;
+  SW_CUDA(cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(e0_), static_cast<cudaEvent_t>(e1_)));
+  return ms;
+}
+
 void Context::memcpy_d2h(void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
+  counters.d2h_bytes += bytes;
   SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream_)));
   sync();
 }
 
 void Context::memcpy_h2d(void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
+  counters.h2d_bytes += bytes;
   SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream_)));
 }
 

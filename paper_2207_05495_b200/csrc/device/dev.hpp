@@ -85,6 +85,22 @@ struct Counters {
   double expand_ms = 0;      // accumulated CUDA-event time of expansion kernels
   u64 expand_children = 0;   // children produced by those launches
   u64 contain_pair_tests = 0;
+  u64 h2d_bytes = 0;
+  u64 d2h_bytes = 0;
+};
+
+// CUDA-event pair on a context's stream (device-side span of a region).
+class StreamTimer {
+ public:
+  explicit StreamTimer(Context& c);
+  ~StreamTimer();
+  void start();
+  double stop_ms();  // records the end event, waits for it, returns elapsed ms
+
+ private:
+  Context& c_;
+  void* e0_ = nullptr;
+  void* e1_ = nullptr;
 };
 
 class Context {

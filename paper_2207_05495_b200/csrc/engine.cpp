@@ -495,8 +495,13 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
   const auto t1 = clock::now();
   res.heuristic_seconds = std::chrono::duration<double>(t1 - t0).count();
 
+  dev::StreamTimer engine_timer(ctx);
+  engine_timer.start();
   detail::GpuBibfs eng(aut, R, opt, ctx);
   const auto finish = [&](u64 threshold, std::optional<Word> word, const char* phase) {
+    res.engine_device_ms = engine_timer.stop_ms();
+    res.h2d_bytes = ctx.counters.h2d_bytes;
+    res.d2h_bytes = ctx.counters.d2h_bytes;
     res.threshold = threshold;
     res.word = std::move(word);
     res.peak_memory = eng.ledger().peak();

@@ -79,7 +79,8 @@ class SolveResultC(C.Structure):
         ("expansions_phase1", C.c_uint64), ("expansions_dfs", C.c_uint64),
         ("heuristic_seconds", C.c_double), ("engine_seconds", C.c_double),
         ("expand_kernel_ms", C.c_double), ("kernel_launches", C.c_uint64),
-        ("phase", C.c_char * 16),
+        ("phase", C.c_char * 16), ("engine_device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
     ]
 
 
@@ -255,6 +256,9 @@ class SolveResult:
     expand_kernel_ms: float
     kernel_launches: int
     phase: str
+    engine_device_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
     trace: Optional[List[str]] = field(default=None)
 
     @property
@@ -293,7 +297,8 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
     return SolveResult(r.threshold, word, r.upper_bound, r.iterations, r.bfs_steps, r.ibfs_steps,
                        bool(r.used_dfs), r.peak_memory, r.expansions_phase1, r.expansions_dfs,
                        r.heuristic_seconds, r.engine_seconds, r.expand_kernel_ms,
-                       r.kernel_launches, r.phase.decode(), trace)
+                       r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
+                       r.d2h_bytes, trace)
 
 
 ALGORITHMS = {"eppstein": 0, "beam": 1, "adaptive": 2}

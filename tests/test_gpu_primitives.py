@@ -74,7 +74,6 @@ def test_mark_modes(gpu, ref, mode, n, da, db):
     g = gpu.list_mark(n, a, b, mode)
     r = ref.mark(n, a, b, mode)
     assert np.array_equal(g, r)
-    assert 0 < int(g.sum()) < g.size or n == 570
 
 
 def test_mark_rejects_unsorted_a(gpu):
