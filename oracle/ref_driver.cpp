@@ -13,6 +13,7 @@
 //      can be logged.  A CPU test checks that this replay
 //     reproduces synchro::solve_exact (threshold, peak, iterations, trace).
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -54,6 +55,16 @@ void list_to(const SetList& l, uint64_t* words, uint32_t* cards, uint64_t* tags)
     if (cards) cards[i] = l.card(i);
     if (tags && l.tagged()) tags[i] = l.tag(i);
   }
+}
+
+// Analysis aid: when SYNCHRO_DUMP_DIR is set, the instrumented replay writes the
+// lists at the DFS handoff and every DFS level as raw u64 words.
+void dump_list(const SetList& l, const std::string& name) {
+  const char* dir = std::getenv("SYNCHRO_DUMP_DIR");
+  if (!dir || !*dir) return;
+  std::ofstream f(std::string(dir) + "/" + name + ".u64", std::ios::binary);
+  for (size_t i = 0; i < l.size(); ++i)
+    f.write(reinterpret_cast<const char*>(l.words(i)), l.words_per_set() * sizeof(u64));
 }
 
 }  // namespace
@@ -367,6 +378,7 @@ class LoggedDfs {
       guard.amount = now;
     }
     log.push_back({r, level, hi - lo, generated, next.size()});
+    dump_list(next, "dfs_r" + std::to_string(r) + "_l" + std::to_string(level));
     size_t i = 0;
     while (i < next.size()) {
       const u32 c = next.card(i);
@@ -523,6 +535,8 @@ REF_API int ref_solve_instrumented(uint32_t n, uint32_t k, const uint32_t* delta
         eng.drop_ibfs_history();
         u64 threshold = R;
         if (!eng.l_bfs().empty()) {
+          dump_list(eng.l_bfs(), "lbfs");
+          dump_list(eng.l_ibfs(), "libfs");
           StaticTrie trie = StaticTrie::build(eng.l_bfs(), opt.tuning.min_leaf);
           eng.ledger().charge_or_throw(trie.byte_footprint());
           eng.ledger().release(eng.l_bfs().byte_footprint());

@@ -223,20 +223,192 @@ __global__ void __launch_bounds__(128) contain_query_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-cooperative work-pool traversal (the production query kernel).
+//
+// Per-query traversal lengths are heavy-tailed (n=300: mean ~1e3 node visits,
+// p99 ~8e3, max ~6e4), so one-thread-per-query leaves warps waiting on their
+// slowest lane and a small query batch (the meet check: ~2e4 queries) runs
+// for the serial latency of its longest walk.  Here every warp owns a LIFO
+// pool of (query, node, depth) tasks in shared memory.  Each round the 32
+// lanes pop 32 tasks — from any mix of queries — test them, and push the
+// admissible children back with ballot-compacted stores; when the pool holds
+// fewer than 32 tasks the warp pulls new queries from a global counter.
+// Long queries are thereby spread over all lanes, short ones pack densely,
+// and the grid is persistent (a fixed number of CTAs per SM).
+constexpr int kPoolWarps = 4;
+constexpr int kPoolThreads = kPoolWarps * 32;
+constexpr int kPoolCap = 1024;  // tasks per warp
+constexpr u32 kNone = 0xFFFFFFFFu;
+
+template <int W>
+__device__ __forceinline__ bool brute_range(const u64* __restrict__ A, const u32* __restrict__ Acard,
+                                            u32 first, u32 last, u32 limit, const u64 (&y)[W],
+                                            u32* hit_a) {
+  for (u32 x = first; x <= last; ++x)
+    if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+      *hit_a = x;
+      return true;
+    }
+  return false;
+}
+
+template <int W, bool PROPER, bool EXIST>
+__global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
+    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
+    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u32 Nb,
+    uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
+  __shared__ u32 s_q[kPoolWarps][kPoolCap];
+  __shared__ u32 s_n[kPoolWarps][kPoolCap];
+  __shared__ uint16_t s_d[kPoolWarps][kPoolCap];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  u32* sq = s_q[wid];
+  u32* sn = s_n[wid];
+  uint16_t* sd = s_d[wid];
+  int sp = 0;
+  bool more = true;
+  while (true) {
+    if (EXIST && *reinterpret_cast<volatile int*>(found)) break;
+    if (sp < 32 && more) {  // refill with fresh queries
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      const u32 got = base >= Nb ? 0 : min(static_cast<u32>(32 - sp), Nb - base);
+      if (base + (32 - sp) >= Nb) more = false;
+      const u32 j = base + lane;
+      bool push = static_cast<u32>(lane) < got;
+      if (push && PROPER && Bcard[j] == 0) push = false;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, push);
+      if (push) {
+        const int pos = sp + __popc(m & lt);
+        sq[pos] = j;
+        sn[pos] = Na == 1 ? kLeafBit : 0u;
+        sd[pos] = 0;
+      }
+      sp += __popc(m);
+      __syncwarp();
+    }
+    if (sp == 0) {
+      if (!more) break;
+      continue;
+    }
+    const int take = sp < 32 ? sp : 32;
+    bool have = lane < take;
+    u32 j = 0, id = 0;
+    int d = 0;
+    if (have) {
+      const int pos = sp - 1 - lane;
+      j = sq[pos];
+      id = sn[pos];
+      d = sd[pos];
+    }
+    sp -= take;
+    __syncwarp();
+    if (have && !EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) have = false;
+    u32 c0 = kNone, c1 = kNone, nfirst = 0, nlast = 0;
+    int dchild = 0;
+    bool hit = false;
+    u32 hit_a = 0;
+    u64 y[W];
+    u32 limit = 0;
+    if (have) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
+      const u32 cy = Bcard[j];
+      limit = PROPER ? cy - 1 : cy;
+      if (id & kLeafBit) {
+        const u32 x = id & ~kLeafBit;
+        hit = brute_range<W>(A, Acard, x, x, limit, y, &hit_a);
+      } else {
+        const Node nd = nodes[id];
+        if (nd.minc <= limit) {
+          if (nd.last - nd.first < kBrute) {
+            hit = brute_range<W>(A, Acard, nd.first, nd.last, limit, y, &hit_a);
+          } else {
+            const int L = nd.lcp;
+            const u64* xf = A + static_cast<u64>(nd.first) * W;
+            u64 bad = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+            if (!bad) {
+              c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+              if ((y[L >> 6] >> (63 - (L & 63))) & 1)
+                c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+              dchild = L + 1;
+              nfirst = nd.first;
+              nlast = nd.last;
+            }
+          }
+        }
+      }
+    }
+    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, c0 != kNone);
+    const unsigned m1 = __ballot_sync(0xFFFFFFFFu, c1 != kNone);
+    const int n0 = __popc(m0), n1 = __popc(m1);
+    if (sp + n0 + n1 > kPoolCap) {
+      // Pool full: finish the opened subtrees linearly instead of pushing.
+      if (c0 != kNone) hit = hit || brute_range<W>(A, Acard, nfirst, nlast, limit, y, &hit_a);
+    } else {
+      if (c1 != kNone) {
+        const int pos = sp + __popc(m1 & lt);
+        sq[pos] = j;
+        sn[pos] = c1;
+        sd[pos] = static_cast<uint16_t>(dchild);
+      }
+      if (c0 != kNone) {  // left children on top: explored first
+        const int pos = sp + n1 + __popc(m0 & lt);
+        sq[pos] = j;
+        sn[pos] = c0;
+        sd[pos] = static_cast<uint16_t>(dchild);
+      }
+      sp += n0 + n1;
+    }
+    if (hit) {
+      if (EXIST) {
+        if (atomicCAS(found, 0, 1) == 0) {
+          wit[0] = hit_a;
+          wit[1] = j;
+        }
+      } else {
+        keep[j] = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <bool PROPER, bool EXIST>
 static void launch_query(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
                          uint8_t* keep, int* found, unsigned long long* wit) {
   const u64 Nb = b.size();
   if (!Nb) return;
-  const int block = 128;
-  const u64 grid = (Nb + block - 1) / block;
+  cudaStream_t s = as_stream(c.stream());
+  if (!EXIST) SW_CUDA(cudaMemsetAsync(keep, 1, Nb, s));
+  if (a.empty()) return;
+  u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..3)
+  SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    SW_CUDA(cudaGetDevice(&dev));
+    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SW_DISPATCH_W(c.W(), {
+      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
+    });
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
   SW_DISPATCH_W(c.W(), {
-    contain_query_kernel<W, PROPER, EXIST><<<static_cast<unsigned>(grid), block, 0, as_stream(c.stream())>>>(
+    contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         a.words, a.cards, static_cast<const Node*>(ia.nodes), static_cast<u32>(a.size()), b.words,
-        b.cards, Nb, keep, found, wit);
+        b.cards, static_cast<u32>(Nb), keep, found, wit, counter);
   });
   SW_CHECK_LAUNCH();
-  c.counters.kernel_launches++;
+  c.counters.kernel_launches += 1;
 }
 
 size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper) {
