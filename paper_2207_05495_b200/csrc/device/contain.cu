@@ -238,21 +238,14 @@ __global__ void __launch_bounds__(128) contain_query_kernel(
 // and the grid is persistent (a fixed number of CTAs per SM).
 constexpr int kPoolWarps = 4;
 constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 1024;  // tasks per warp
+constexpr int kPoolCap = 768;  // tasks per warp
+constexpr int kPoolBrute = 16; // ranges of <= this many keys are scanned cooperatively
 constexpr u32 kNone = 0xFFFFFFFFu;
 
-template <int W>
-__device__ __forceinline__ bool brute_range(const u64* __restrict__ A, const u32* __restrict__ Acard,
-                                            u32 first, u32 last, u32 limit, const u64 (&y)[W],
-                                            u32* hit_a) {
-  for (u32 x = first; x <= last; ++x)
-    if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-      *hit_a = x;
-      return true;
-    }
-  return false;
-}
-
+// A task is (query j, tree node id | kLeafBit, first key of the node's range,
+// next bit to check).  Carrying `first` lets the node record, the node's
+// first key (prefix check), the query row and the flags load concurrently:
+// one memory round trip per task.
 template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
@@ -260,12 +253,15 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
+  __shared__ u32 s_f[kPoolWarps][kPoolCap];
   __shared__ uint16_t s_d[kPoolWarps][kPoolCap];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1;
+  const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
   u32* sq = s_q[wid];
   u32* sn = s_n[wid];
+  u32* sf = s_f[wid];
   uint16_t* sd = s_d[wid];
+  const u32 root_id = Na == 1 ? kLeafBit : 0u;
   int sp = 0;
   bool more = true;
   while (true) {
@@ -273,17 +269,18 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     if (sp < 32 && more) {  // refill with fresh queries
       u32 base = 0;
       if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
-      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      base = __shfl_sync(FULL, base, 0);
       const u32 got = base >= Nb ? 0 : min(static_cast<u32>(32 - sp), Nb - base);
       if (base + (32 - sp) >= Nb) more = false;
       const u32 j = base + lane;
       bool push = static_cast<u32>(lane) < got;
       if (push && PROPER && Bcard[j] == 0) push = false;
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, push);
+      const unsigned m = __ballot_sync(FULL, push);
       if (push) {
         const int pos = sp + __popc(m & lt);
         sq[pos] = j;
-        sn[pos] = Na == 1 ? kLeafBit : 0u;
+        sn[pos] = root_id;
+        sf[pos] = 0;
         sd[pos] = 0;
       }
       sp += __popc(m);
@@ -295,74 +292,141 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     }
     const int take = sp < 32 ? sp : 32;
     bool have = lane < take;
-    u32 j = 0, id = 0;
+    u32 j = 0, id = 0, first = 0;
     int d = 0;
     if (have) {
       const int pos = sp - 1 - lane;
       j = sq[pos];
       id = sn[pos];
+      first = sf[pos];
       d = sd[pos];
     }
     sp -= take;
     __syncwarp();
-    if (have && !EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) have = false;
-    u32 c0 = kNone, c1 = kNone, nfirst = 0, nlast = 0;
-    int dchild = 0;
-    bool hit = false;
-    u32 hit_a = 0;
-    u64 y[W];
-    u32 limit = 0;
+
+    // ---- one concurrent round of loads
+    u64 y[W], xf[W];
+    u32 cy = 0, kcard = 0;
+    Node nd{};
+    bool alive = have;
     if (have) {
 #pragma unroll
       for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
-      const u32 cy = Bcard[j];
-      limit = PROPER ? cy - 1 : cy;
-      if (id & kLeafBit) {
-        const u32 x = id & ~kLeafBit;
-        hit = brute_range<W>(A, Acard, x, x, limit, y, &hit_a);
-      } else {
-        const Node nd = nodes[id];
-        if (nd.minc <= limit) {
-          if (nd.last - nd.first < kBrute) {
-            hit = brute_range<W>(A, Acard, nd.first, nd.last, limit, y, &hit_a);
-          } else {
-            const int L = nd.lcp;
-            const u64* xf = A + static_cast<u64>(nd.first) * W;
-            u64 bad = 0;
 #pragma unroll
-            for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-            if (!bad) {
-              c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-              if ((y[L >> 6] >> (63 - (L & 63))) & 1)
-                c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-              dchild = L + 1;
-              nfirst = nd.first;
-              nlast = nd.last;
+      for (int w = 0; w < W; ++w) xf[w] = A[static_cast<u64>(first) * W + w];
+      cy = Bcard[j];
+      if (id & kLeafBit) kcard = Acard[first];
+      else nd = nodes[id];
+      if (!EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) alive = false;
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
+    }
+    const u32 limit = PROPER ? cy - 1 : cy;
+
+    // ---- evaluate the task
+    bool hit = false;
+    u32 hit_a = 0;
+    u32 c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
+    bool brute = false;
+    int dchild = 0;
+    if (alive) {
+      if (id & kLeafBit) {
+        if (kcard <= limit && is_subset<W>(xf, y)) {
+          hit = true;
+          hit_a = first;
+        }
+      } else if (nd.minc <= limit) {
+        if (nd.last - nd.first < kPoolBrute) {
+          brute = true;
+          bf = nd.first;
+          bl = nd.last;
+        } else {
+          const int L = nd.lcp;
+          u64 bad = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+          if (!bad) {
+            const bool lleaf = nd.split == nd.first, rleaf = nd.split + 1 == nd.last;
+            c0 = lleaf ? (kLeafBit | nd.first) : nd.split;
+            f0 = nd.first;
+            if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
+              c1 = rleaf ? (kLeafBit | nd.last) : nd.split + 1;
+              f1 = nd.split + 1;
             }
+            dchild = L + 1;
+            bf = nd.first;
+            bl = nd.last;
           }
         }
       }
     }
-    const unsigned m0 = __ballot_sync(0xFFFFFFFFu, c0 != kNone);
-    const unsigned m1 = __ballot_sync(0xFFFFFFFFu, c1 != kNone);
+
+    // ---- push children (LIFO; left on top)
+    const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
+    const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
     const int n0 = __popc(m0), n1 = __popc(m1);
     if (sp + n0 + n1 > kPoolCap) {
-      // Pool full: finish the opened subtrees linearly instead of pushing.
-      if (c0 != kNone) hit = hit || brute_range<W>(A, Acard, nfirst, nlast, limit, y, &hit_a);
+      if (c0 != kNone) brute = true;  // pool full: scan the opened range instead
     } else {
       if (c1 != kNone) {
         const int pos = sp + __popc(m1 & lt);
         sq[pos] = j;
         sn[pos] = c1;
+        sf[pos] = f1;
         sd[pos] = static_cast<uint16_t>(dchild);
       }
-      if (c0 != kNone) {  // left children on top: explored first
+      if (c0 != kNone) {
         const int pos = sp + n1 + __popc(m0 & lt);
         sq[pos] = j;
         sn[pos] = c0;
+        sf[pos] = f0;
         sd[pos] = static_cast<uint16_t>(dchild);
       }
       sp += n0 + n1;
+    }
+    __syncwarp();
+
+    // ---- cooperative scan of small ranges: all (range, key) pairs of the warp
+    // are flattened and spread over the lanes, 32 independent key tests per pass.
+    const u32 cnt = brute ? bl - bf + 1 : 0;
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const u32 total = __shfl_sync(FULL, incl, 31);
+    const u32 excl = incl - cnt;
+    for (u32 base = 0; base < total; base += 32) {
+      const u32 t = base + lane;
+      int owner = 0;
+#pragma unroll
+      for (int s = 16; s; s >>= 1) {
+        const u32 v = __shfl_sync(FULL, incl, owner + s - 1);
+        if (v <= t) owner += s;
+      }
+      owner = owner > 31 ? 31 : owner;
+      const u32 o_excl = __shfl_sync(FULL, excl, owner);
+      const u32 o_bf = __shfl_sync(FULL, bf, owner);
+      const u32 o_j = __shfl_sync(FULL, j, owner);
+      const u32 o_lim = __shfl_sync(FULL, limit, owner);
+      u64 oy[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) oy[w] = __shfl_sync(FULL, y[w], owner);
+      if (t < total) {
+        const u32 key = o_bf + (t - o_excl);
+        if (Acard[key] <= o_lim && is_subset<W>(A + static_cast<u64>(key) * W, oy)) {
+          if (EXIST) {
+            if (atomicCAS(found, 0, 1) == 0) {
+              wit[0] = key;
+              wit[1] = o_j;
+            }
+          } else {
+            keep[o_j] = 0;
+          }
+        }
+      }
     }
     if (hit) {
       if (EXIST) {

@@ -5,7 +5,7 @@ rows = list(csv.reader(open(path)))
 hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 hdr = rows[hdr_i]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for r in rows[hdr_i + 1:]:
     if len(r) <= vi:
