@@ -236,9 +236,9 @@ __global__ void __launch_bounds__(128) contain_query_kernel(
 // fewer than 32 tasks the warp pulls new queries from a global counter.
 // Long queries are thereby spread over all lanes, short ones pack densely,
 // and the grid is persistent (a fixed number of CTAs per SM).
-constexpr int kPoolWarps = 4;
+constexpr int kPoolWarps = 6;
 constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 768;  // tasks per warp
+constexpr int kPoolCap = 512;  // tasks per warp
 constexpr int kPoolBrute = 16; // ranges of <= this many keys are scanned cooperatively
 constexpr u32 kNone = 0xFFFFFFFFu;
 
@@ -499,13 +499,166 @@ std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainInde
   return out;
 }
 
+// ------------------------------------------------------- state relabelling
+__global__ void state_hist_kernel(const u64* __restrict__ words, u64 count, u32 W, u32 n,
+                                  u32* __restrict__ hist) {
+  extern __shared__ u32 sh[];
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count * W;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 bits = words[i];
+    const u32 base = static_cast<u32>(i % W) * 64;
+    while (bits) {
+      const int b = __clzll(bits);
+      bits &= ~(u64{1} << (63 - b));
+      atomicAdd(&sh[base + b], 1u);
+    }
+  }
+  __syncthreads();
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x)
+    if (sh[q]) atomicAdd(&hist[q], sh[q]);
+}
+
+template <int W>
+__global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
+                               u32 n, const uint16_t* __restrict__ g_pos, u64* __restrict__ dst,
+                               u32* __restrict__ dcard) {
+  extern __shared__ uint16_t s_pos[];
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x) s_pos[q] = g_pos[q];
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      u64 bits = src[i * W + w];
+      while (bits) {
+        const int b = __clzll(bits);
+        bits &= ~(u64{1} << (63 - b));
+        const u32 t = s_pos[w * 64 + b];
+        const u64 m = u64{1} << (63 - (t & 63));
+#pragma unroll
+        for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == (t >> 6)) ? m : 0;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) dst[i * W + w] = acc[w];
+    dcard[i] = scard[i];
+  }
+}
+
+PermIndex::~PermIndex() {
+  if (ctx) {
+    try {
+      ctx->free(orig);
+      ctx->free(state_pos);
+    } catch (...) {
+    }
+  }
+}
+PermIndex::PermIndex(PermIndex&& o) noexcept { *this = std::move(o); }
+PermIndex& PermIndex::operator=(PermIndex&& o) noexcept {
+  if (this != &o) {
+    if (ctx) {
+      ctx->free(orig);
+      ctx->free(state_pos);
+    }
+    ctx = o.ctx;
+    sorted = std::move(o.sorted);
+    orig = o.orig;
+    state_pos = o.state_pos;
+    tree = std::move(o.tree);
+    o.orig = nullptr;
+    o.state_pos = nullptr;
+  }
+  return *this;
+}
+
+DList relabel(Context& c, const DList& l, const PermIndex& p) {
+  DList out(&c, l.size(), false);
+  out.set_size(l.size());
+  if (l.empty()) return out;
+  SW_DISPATCH_W(c.W(), {
+    relabel_kernel<W><<<grid_for(l.size(), 256, 148 * 8), 256, c.n() * 2, as_stream(c.stream())>>>(
+        l.words, l.cards, l.size(), c.n(), p.state_pos, out.words, out.cards);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+  return out;
+}
+
+PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
+  PermIndex p;
+  p.ctx = &c;
+  const u32 n = c.n();
+  cudaStream_t s = as_stream(c.stream());
+  std::vector<uint16_t> pos(n);
+  for (u32 q = 0; q < n; ++q) pos[q] = static_cast<uint16_t>(q);
+  if (order != StateOrder::Natural && !a.empty()) {
+    u32* hist = static_cast<u32*>(c.alloc(n * 4));
+    SW_CUDA(cudaMemsetAsync(hist, 0, n * 4, s));
+    state_hist_kernel<<<grid_for(a.size() * c.W(), 256, 148 * 2), 256, n * 4, s>>>(a.words, a.size(), c.W(), n,
+                                                                                   hist);
+    SW_CHECK_LAUNCH();
+    std::vector<u32> h(n);
+    c.memcpy_d2h(h.data(), hist, n * 4);
+    c.free(hist);
+    std::vector<u32> ord(n);
+    for (u32 q = 0; q < n; ++q) ord[q] = q;
+    if (order == StateOrder::FreqDesc)
+      std::stable_sort(ord.begin(), ord.end(), [&](u32 x, u32 y) { return h[x] > h[y]; });
+    else
+      std::stable_sort(ord.begin(), ord.end(), [&](u32 x, u32 y) { return h[x] < h[y]; });
+    for (u32 i = 0; i < n; ++i) pos[ord[i]] = static_cast<uint16_t>(i);
+  }
+  p.state_pos = static_cast<uint16_t*>(c.alloc(n * 2));
+  c.memcpy_h2d(p.state_pos, pos.data(), n * 2);
+  p.sorted = std::make_unique<DList>(relabel(c, a, p));
+  p.orig = static_cast<u32*>(c.alloc(std::max<size_t>(a.size(), 1) * 4));
+  if (a.size() > 1) {
+    const u32* perm = sort_perm(c, *p.sorted, false);
+    SW_CUDA(cudaMemcpyAsync(p.orig, perm, a.size() * 4, cudaMemcpyDeviceToDevice, s));
+    compact_flags(c, *p.sorted, nullptr, p.orig);
+  } else if (a.size() == 1) {
+    SW_CUDA(cudaMemsetAsync(p.orig, 0, 4, s));
+  }
+  p.tree = build_index(c, *p.sorted);
+  return p;
+}
+
+bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
+  if (!p.sorted || p.sorted->empty() || b.empty()) return false;
+  const DList rb = relabel(c, b, p);
+  Witness tw;
+  if (!exists_subset(c, *p.sorted, p.tree, rb, &tw)) return false;
+  if (w) {
+    u32 o = 0;
+    c.memcpy_d2h(&o, p.orig + tw.a_index, 4);
+    w->a_index = o;
+    w->b_index = tw.b_index;
+  }
+  return true;
+}
+
+size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper) {
+  if (b.empty() || !p.sorted || p.sorted->empty()) return 0;
+  const DList rb = relabel(c, b, p);
+  const size_t before = b.size();
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+  if (proper)
+    launch_query<true, false>(c, *p.sorted, p.tree, rb, keep, nullptr, nullptr);
+  else
+    launch_query<false, false>(c, *p.sorted, p.tree, rb, keep, nullptr, nullptr);
+  return before - compact_flags(c, b, keep, nullptr);
+}
+
 size_t self_reduce_minimal(Context& c, DList& l) {
   if (l.size() <= 1) return 0;
-  const ContainIndex ix = build_index(c, l);
-  const size_t before = l.size();
-  auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
-  launch_query<true, false>(c, l, ix, l, keep, nullptr, nullptr);
-  return before - compact_flags(c, l, keep, nullptr);
+  const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
+  return remove_supersets(c, p, l, /*proper=*/true);
 }
 
 bool exists_subset(Context& c, const DList& a, const ContainIndex& ia, const DList& b, Witness* w) {

@@ -166,6 +166,30 @@ ContainIndex build_index(Context& c, const DList& a);  // a lex-sorted unique
 // Removes every b element that is a superset (proper: strict superset) of
 // some a element; b keeps its order.  Returns #removed.
 size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper);
+// Containment index over A with the states relabelled so that the radix tree
+// splits first on the states that prune best for the expected queries:
+//   FreqDesc — most frequent state of A first (queries sparser than A:
+//              meet check, DFS trie query; ~2.5x fewer visits at n=300),
+//   FreqAsc  — rarest first (self-reduction; ~1.3x fewer visits).
+// The relabelling is a bijection, so containment (and every size) is
+// unchanged; witness indices are mapped back to A's original positions.
+enum class StateOrder { Natural, FreqDesc, FreqAsc };
+struct PermIndex {
+  PermIndex() = default;
+  ~PermIndex();
+  PermIndex(PermIndex&&) noexcept;
+  PermIndex& operator=(PermIndex&&) noexcept;
+  Context* ctx = nullptr;
+  std::unique_ptr<DList> sorted;  // relabelled, lex-sorted unique copy of A
+  u32* orig = nullptr;            // sorted position -> index in A
+  uint16_t* state_pos = nullptr;  // state q -> relabelled position
+  ContainIndex tree;
+};
+PermIndex build_perm_index(Context& c, const DList& a, StateOrder order);
+DList relabel(Context& c, const DList& l, const PermIndex& p);  // same order, untagged
+bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w);
+size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper);
+
 // keep[j] = 1 iff b[j] is not a (proper) superset of any a element.
 std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
                                    bool proper);

@@ -139,8 +139,12 @@ void GpuBibfs::drop_ibfs_history() {
   ibfs_hist_dropped_ = true;
 }
 
-const dev::ContainIndex& GpuBibfs::bfs_index() {
-  if (!lbfs_index_) lbfs_index_ = std::make_unique<dev::ContainIndex>(dev::build_index(ctx_, *lbfs_));
+// L_BFS relabelled most-frequent-state-first: the meet check and the DFS
+// query are subset queries from sparser sets, where that order prunes best.
+const dev::PermIndex& GpuBibfs::bfs_index() {
+  if (!lbfs_index_)
+    lbfs_index_ = std::make_unique<dev::PermIndex>(
+        dev::build_perm_index(ctx_, *lbfs_, dev::StateOrder::FreqDesc));
   return *lbfs_index_;
 }
 
@@ -264,11 +268,11 @@ void GpuBibfs::perform(StepKind kind) {
 }
 
 // Meet: is some X in L_BFS a subset of some Y in L_IBFS?
-bool GpuBibfs::meet() { return dev::exists_subset(ctx_, *lbfs_, bfs_index(), *libfs_, nullptr); }
+bool GpuBibfs::meet() { return dev::exists_subset(ctx_, bfs_index(), *libfs_, nullptr); }
 
 bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
   dev::Witness w;
-  if (!dev::exists_subset(ctx_, *lbfs_, bfs_index(), *libfs_, &w)) return false;
+  if (!dev::exists_subset(ctx_, bfs_index(), *libfs_, &w)) return false;
   *bfs_index_out = w.a_index;
   *ibfs_tag = dev::read_tag(ctx_, *libfs_, w.b_index);
   return true;
@@ -283,7 +287,7 @@ namespace {
 // query against L_BFS are device kernels.
 class DfsRunner {
  public:
-  DfsRunner(dev::Context& c, const DList& lbfs, const dev::ContainIndex& index,
+  DfsRunner(dev::Context& c, const DList& lbfs, const dev::PermIndex& index,
             MemoryLedger& ledger, const EngineTuning& t, const Deadline& deadline, bool tracking,
             std::vector<std::array<u64, 5>>* log)
       : c_(c), lbfs_(lbfs), index_(index), ledger_(ledger), t_(t), deadline_(deadline),
@@ -350,7 +354,7 @@ class DfsRunner {
     }
     if (log_) log_->push_back({r, level, hi - lo, generated, next.size()});
     dev::Witness w;
-    if (dev::exists_subset(c_, lbfs_, index_, next, tracking_ ? &w : nullptr)) {
+    if (dev::exists_subset(c_, index_, next, tracking_ ? &w : nullptr)) {
       bound_ = r;
       if (tracking_) record_find(w, next, parent);
       return;
@@ -382,7 +386,7 @@ class DfsRunner {
 
   dev::Context& c_;
   const DList& lbfs_;
-  const dev::ContainIndex& index_;
+  const dev::PermIndex& index_;
   MemoryLedger& ledger_;
   const EngineTuning& t_;
   const Deadline& deadline_;
@@ -406,7 +410,7 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   const u64 trie_bytes = list_footprint(n_, lbfs_i_.size) + nodes * 24;
   ledger_.charge_or_throw(trie_bytes);
   ledger_.release(list_footprint(n_, lbfs_i_.size));
-  const dev::ContainIndex& index = bfs_index();
+  const dev::PermIndex& index = bfs_index();
   DfsRunner dfs(ctx_, *lbfs_, index, ledger_, opt_.tuning, deadline_, opt_.track_word, log);
   const u64 final_bound = dfs.run(*libfs_, r, R_);
   if (find) *find = dfs.find();

@@ -25,6 +25,7 @@ namespace dev {
 class Context;
 class DList;
 struct ContainIndex;
+struct PermIndex;
 }  // namespace dev
 
 enum class Schedule { Auto, BfsOnly, IbfsOnly, DfsImmediate };
@@ -126,7 +127,7 @@ class GpuBibfs {
   void charge_layer(size_t parents);
   void shrink_charge(size_t now_size);
   void merge_history(dev::DList& h, Info& hi, const dev::DList& add);
-  const dev::ContainIndex& bfs_index();
+  const dev::PermIndex& bfs_index();
 
   const Automaton& aut_;
   const SolveOptions& opt_;
@@ -137,7 +138,7 @@ class GpuBibfs {
   u64 R_;
   u64 r_ = 0;
   std::unique_ptr<dev::DList> lbfs_, libfs_, hbfs_, hibfs_c_;
-  std::unique_ptr<dev::ContainIndex> lbfs_index_;
+  std::unique_ptr<dev::PermIndex> lbfs_index_;
   Info lbfs_i_, libfs_i_, hbfs_i_, hibfs_i_;
   size_t h_bfs_last_reduced_ = 1, h_ibfs_last_reduced_ = 1;
   bool bfs_hist_dropped_ = false, ibfs_hist_dropped_ = false;
