@@ -4,20 +4,19 @@
 //
 // The reference splits a lex-sorted A on bit d by binary search and
 // partitions B in place, recursively — inherently sequential.  Here the
-// lex-sorted unique A is turned into an explicit binary radix (Patricia) tree
-// in parallel (Karras, HPG 2012: node i of N-1 internal nodes is found from
-// longest-common-prefix lengths of neighbouring keys by binary search, no
-// inter-thread communication), each node annotated with its subtree's
-// minimum cardinality.  Every query set y is then handled by one thread that
-// walks the tree depth-first:
+// lex-sorted unique A becomes an explicit binary radix (Patricia) tree built
+// in parallel (Karras, HPG 2012: internal node i is found from the longest
+// common prefixes of neighbouring keys by binary search, no inter-thread
+// communication), each node annotated with its subtree's min cardinality.
+// A query y walks the tree depth-first:
 //   * a node's keys agree on bits < lcp; bits [d, lcp) of that common prefix
 //     must lie in y (else the subtree is dead);
 //   * at the split bit L the 0-child is always admissible, the 1-child only if
 //     y has state L (exactly the reference's "ones side recurses with B_1");
 //   * subtrees whose min cardinality exceeds |y| (|y|-1 for proper) are cut —
 //     the reference's per-pair card filter lifted to whole subtrees;
-//   * ranges of <= kBrute keys are scanned linearly (contiguous rows).
-// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} is independent of
+//   * ranges of <= kPoolBrute keys are scanned (warp-cooperatively).
+// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} does not depend on the
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
 
@@ -34,9 +33,8 @@ struct __align__(16) Node {
   uint16_t minc;    // min cardinality in the range
 };
 
+
 constexpr u32 kLeafBit = 0x80000000u;
-constexpr int kBrute = 12;
-constexpr int kStack = 64;
 
 template <int W>
 __device__ __forceinline__ int key_delta(const u64* __restrict__ A, long long N, long long i,
@@ -129,6 +127,30 @@ ContainIndex build_index(Context& c, const DList& a) {
   return ix;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-cooperative work-pool traversal.
+//
+// Per-query walks are heavy-tailed (n=300: mean ~1e3 node visits, p99 ~8e3,
+// max ~6e4), so one-thread-per-query leaves warps waiting on their slowest
+// lane and a small batch (the meet check: ~2e4 queries) runs for the serial
+// latency of its longest walk.  Here every warp owns a LIFO pool of tasks
+// (query j, node, first key of the node's range, next bit d, |y|) in shared
+// memory.  Each round the lanes pop up to 32 tasks from any mix of queries,
+// evaluate them and push the admissible children with ballot-compacted
+// stores; when fewer than 32 tasks remain the warp pulls new queries from a
+// global counter (persistent grid).  Loads are staged to keep the L1/TEX
+// pipe (the measured bottleneck) light: the node record first, then only the
+// words of y and of the node's first key that the prefix check touches.
+// Small ranges are scanned cooperatively: all (range, key) pairs of the warp
+// are flattened over the lanes (consecutive keys → coalesced rows) with the
+// owner's y broadcast by shuffles.
+constexpr int kPoolWarps = 6;
+constexpr int kPoolThreads = kPoolWarps * 32;
+constexpr int kPoolCap = 480;   // tasks per warp (static smem <= 48 KB per block)
+constexpr int kPoolBrute = 16;  // ranges of <= this many keys are scanned
+constexpr int kHitSlots = 64;   // per-warp table of recently hit queries (MARK mode)
+constexpr u32 kNone = 0xFFFFFFFFu;
+
 template <int W>
 __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (&y)[W]) {
   u64 acc = 0;
@@ -137,115 +159,6 @@ __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (
   return acc == 0;
 }
 
-// One thread per query y.  EXIST: stop everything at the first hit (meet
-// check / DFS trie query); otherwise write keep[j] = !hit.
-template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(128) contain_query_kernel(
-    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
-    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u64 Nb,
-    uint8_t* __restrict__ keep, int* found, unsigned long long* wit) {
-  const u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-  if (j >= Nb) return;
-  if (EXIST && *reinterpret_cast<volatile int*>(found)) return;
-  u64 y[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) y[w] = B[j * W + w];
-  const u32 cy = Bcard[j];
-  bool hit = false;
-  u32 hit_a = 0;
-  if (Na > 0 && !(PROPER && cy == 0)) {
-    const u32 limit = PROPER ? cy - 1 : cy;
-    u32 st_id[kStack];
-    uint16_t st_d[kStack];
-    int sp = 0;
-    st_id[sp] = Na == 1 ? kLeafBit : 0u;
-    st_d[sp++] = 0;
-    u32 iter = 0;
-    while (sp > 0 && !hit) {
-      if (EXIST && ((++iter & 63) == 0) && *reinterpret_cast<volatile int*>(found)) break;
-      --sp;
-      const u32 id = st_id[sp];
-      const int d = st_d[sp];
-      if (id & kLeafBit) {
-        const u32 x = id & ~kLeafBit;
-        if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-          hit = true;
-          hit_a = x;
-        }
-        continue;
-      }
-      const Node nd = nodes[id];
-      if (nd.minc > limit) continue;
-      if (nd.last - nd.first < kBrute) {
-        for (u32 x = nd.first; x <= nd.last; ++x)
-          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-            hit = true;
-            hit_a = x;
-            break;
-          }
-        continue;
-      }
-      const int L = nd.lcp;
-      // Bits [d, L) are common to the whole range: they must lie in y.
-      const u64* xf = A + static_cast<u64>(nd.first) * W;
-      u64 bad = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-      if (bad) continue;
-      const u32 left = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-      const u32 right = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-      const bool y_has_L = (y[L >> 6] >> (63 - (L & 63))) & 1;
-      if (sp + 2 > kStack) {
-        // Stack exhausted (very deep tree): finish this subtree linearly.
-        for (u32 x = nd.first; x <= nd.last; ++x)
-          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-            hit = true;
-            hit_a = x;
-            break;
-          }
-        continue;
-      }
-      if (y_has_L) {
-        st_id[sp] = right;
-        st_d[sp++] = static_cast<uint16_t>(L + 1);
-      }
-      st_id[sp] = left;
-      st_d[sp++] = static_cast<uint16_t>(L + 1);
-    }
-  }
-  if (EXIST) {
-    if (hit && atomicCAS(found, 0, 1) == 0) {
-      wit[0] = hit_a;
-      wit[1] = j;
-    }
-  } else {
-    keep[j] = hit ? 0 : 1;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-cooperative work-pool traversal (the production query kernel).
-//
-// Per-query traversal lengths are heavy-tailed (n=300: mean ~1e3 node visits,
-// p99 ~8e3, max ~6e4), so one-thread-per-query leaves warps waiting on their
-// slowest lane and a small query batch (the meet check: ~2e4 queries) runs
-// for the serial latency of its longest walk.  Here every warp owns a LIFO
-// pool of (query, node, depth) tasks in shared memory.  Each round the 32
-// lanes pop 32 tasks — from any mix of queries — test them, and push the
-// admissible children back with ballot-compacted stores; when the pool holds
-// fewer than 32 tasks the warp pulls new queries from a global counter.
-// Long queries are thereby spread over all lanes, short ones pack densely,
-// and the grid is persistent (a fixed number of CTAs per SM).
-constexpr int kPoolWarps = 6;
-constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 512;  // tasks per warp
-constexpr int kPoolBrute = 16; // ranges of <= this many keys are scanned cooperatively
-constexpr u32 kNone = 0xFFFFFFFFu;
-
-// A task is (query j, tree node id | kLeafBit, first key of the node's range,
-// next bit to check).  Carrying `first` lets the node record, the node's
-// first key (prefix check), the query row and the flags load concurrently:
-// one memory round trip per task.
 template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
@@ -254,13 +167,17 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
-  __shared__ uint16_t s_d[kPoolWarps][kPoolCap];
+  __shared__ u32 s_dc[kPoolWarps][kPoolCap];  // d | |y| << 16
+  __shared__ u32 s_hit[kPoolWarps][kHitSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
   u32* sq = s_q[wid];
   u32* sn = s_n[wid];
   u32* sf = s_f[wid];
-  uint16_t* sd = s_d[wid];
+  u32* sdc = s_dc[wid];
+  u32* shit = s_hit[wid];
+  for (int i = lane; i < kHitSlots; i += 32) shit[i] = kNone;
+  __syncwarp();
   const u32 root_id = Na == 1 ? kLeafBit : 0u;
   int sp = 0;
   bool more = true;
@@ -274,14 +191,15 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       if (base + (32 - sp) >= Nb) more = false;
       const u32 j = base + lane;
       bool push = static_cast<u32>(lane) < got;
-      if (push && PROPER && Bcard[j] == 0) push = false;
+      const u32 cy = push ? Bcard[j] : 0;
+      if (PROPER && cy == 0) push = false;
       const unsigned m = __ballot_sync(FULL, push);
       if (push) {
         const int pos = sp + __popc(m & lt);
         sq[pos] = j;
         sn[pos] = root_id;
         sf[pos] = 0;
-        sd[pos] = 0;
+        sdc[pos] = cy << 16;
       }
       sp += __popc(m);
       __syncwarp();
@@ -291,104 +209,113 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       continue;
     }
     const int take = sp < 32 ? sp : 32;
-    bool have = lane < take;
-    u32 j = 0, id = 0, first = 0;
-    int d = 0;
+    const bool have = lane < take;
+    u32 j = 0, id = 0, first = 0, dc = 0;
     if (have) {
       const int pos = sp - 1 - lane;
       j = sq[pos];
       id = sn[pos];
       first = sf[pos];
-      d = sd[pos];
+      dc = sdc[pos];
     }
     sp -= take;
     __syncwarp();
-
-    // ---- one concurrent round of loads
-    u64 y[W], xf[W];
-    u32 cy = 0, kcard = 0;
-    Node nd{};
-    bool alive = have;
-    if (have) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
-#pragma unroll
-      for (int w = 0; w < W; ++w) xf[w] = A[static_cast<u64>(first) * W + w];
-      cy = Bcard[j];
-      if (id & kLeafBit) kcard = Acard[first];
-      else nd = nodes[id];
-      if (!EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) alive = false;
-    } else {
-#pragma unroll
-      for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
-    }
+    const int d = static_cast<int>(dc & 0xFFFF);
+    const u32 cy = dc >> 16;
     const u32 limit = PROPER ? cy - 1 : cy;
+    bool alive = have && !(!EXIST && shit[j % kHitSlots] == j);
+    const bool is_leaf = (id & kLeafBit) != 0;
 
-    // ---- evaluate the task
+    // ---- stage 1: node record (internal) or key cardinality (leaf)
+    Node nd{};
+    u32 kcard = 0;
+    if (alive) {
+      if (is_leaf) kcard = Acard[first];
+      else nd = nodes[id];
+    }
+    bool brute = false, check = false;
+    int L = 0;
+    if (alive) {
+      if (is_leaf) {
+        alive = kcard <= limit;
+      } else if (nd.minc > limit) {
+        alive = false;
+      } else if (nd.last - nd.first < kPoolBrute) {
+        brute = true;
+      } else {
+        check = true;
+        L = nd.lcp;
+      }
+    }
+    // ---- stage 2: only the row words that are needed
+    const bool full_y = alive && (is_leaf || brute);
+    const int ylo = d >> 6, yhi = L >> 6, xhi = (L - 1) >> 6;
+    u64 y[W], xf[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      y[w] = (full_y || (check && w >= ylo && w <= yhi)) ? B[static_cast<u64>(j) * W + w] : 0;
+      xf[w] = ((alive && is_leaf) || (check && L > d && w >= ylo && w <= xhi))
+                  ? A[static_cast<u64>(first) * W + w]
+                  : 0;
+    }
+
     bool hit = false;
     u32 hit_a = 0;
     u32 c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
-    bool brute = false;
-    int dchild = 0;
-    if (alive) {
-      if (id & kLeafBit) {
-        if (kcard <= limit && is_subset<W>(xf, y)) {
-          hit = true;
-          hit_a = first;
-        }
-      } else if (nd.minc <= limit) {
-        if (nd.last - nd.first < kPoolBrute) {
-          brute = true;
-          bf = nd.first;
-          bl = nd.last;
-        } else {
-          const int L = nd.lcp;
-          u64 bad = 0;
+    if (alive && is_leaf && is_subset<W>(xf, y)) {
+      hit = true;
+      hit_a = first;
+    }
+    if (brute) {
+      bf = nd.first;
+      bl = nd.last;
+    }
+    if (check) {
+      u64 bad = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-          if (!bad) {
-            const bool lleaf = nd.split == nd.first, rleaf = nd.split + 1 == nd.last;
-            c0 = lleaf ? (kLeafBit | nd.first) : nd.split;
-            f0 = nd.first;
-            if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
-              c1 = rleaf ? (kLeafBit | nd.last) : nd.split + 1;
-              f1 = nd.split + 1;
-            }
-            dchild = L + 1;
-            bf = nd.first;
-            bl = nd.last;
-          }
+      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+      if (!bad) {
+        c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+        f0 = nd.first;
+        if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
+          c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+          f1 = nd.split + 1;
         }
+        bf = nd.first;
+        bl = nd.last;
       }
     }
 
     // ---- push children (LIFO; left on top)
+    const u32 cdc = (cy << 16) | static_cast<u32>(L + 1);
     const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
     const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
     const int n0 = __popc(m0), n1 = __popc(m1);
     if (sp + n0 + n1 > kPoolCap) {
-      if (c0 != kNone) brute = true;  // pool full: scan the opened range instead
+      if (c0 != kNone) {  // pool full: scan the opened range instead
+        brute = true;
+#pragma unroll
+        for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
+      }
     } else {
       if (c1 != kNone) {
         const int pos = sp + __popc(m1 & lt);
         sq[pos] = j;
         sn[pos] = c1;
         sf[pos] = f1;
-        sd[pos] = static_cast<uint16_t>(dchild);
+        sdc[pos] = cdc;
       }
       if (c0 != kNone) {
         const int pos = sp + n1 + __popc(m0 & lt);
         sq[pos] = j;
         sn[pos] = c0;
         sf[pos] = f0;
-        sd[pos] = static_cast<uint16_t>(dchild);
+        sdc[pos] = cdc;
       }
       sp += n0 + n1;
     }
-    __syncwarp();
 
-    // ---- cooperative scan of small ranges: all (range, key) pairs of the warp
-    // are flattened and spread over the lanes, 32 independent key tests per pass.
+    // ---- cooperative scan of small ranges
     const u32 cnt = brute ? bl - bf + 1 : 0;
     u32 incl = cnt;
 #pragma unroll
@@ -424,6 +351,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
             }
           } else {
             keep[o_j] = 0;
+            shit[o_j % kHitSlots] = o_j;
           }
         }
       }
@@ -436,6 +364,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
         }
       } else {
         keep[j] = 0;
+        shit[j % kHitSlots] = j;
       }
     }
     __syncwarp();

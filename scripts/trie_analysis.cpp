@@ -41,6 +41,7 @@ struct Counter {
   std::vector<u64> per;
 };
 static bool PROPER = false;
+static size_t BRUTE = 12;
 
 struct Sorted {
   std::vector<u64> w;
@@ -81,7 +82,7 @@ void query(const Sorted& A, const std::vector<std::vector<u32>>& rmq, const u64*
     st.pop_back();
     ++c.nodes;
     if (rmin(f.lo, f.hi) > cy - (PROPER ? 1 : 0)) continue;
-    if (f.hi - f.lo <= 12) {
+    if (f.hi - f.lo <= BRUTE) {
       for (size_t i = f.lo; i < f.hi; ++i) {
         ++c.pairs;
         if (A.card[i] > cy - (PROPER ? 1 : 0)) continue;
@@ -114,6 +115,7 @@ int main(int argc, char** argv) {
   auto B0 = load(argv[3]);
   size_t sample = argc > 4 ? std::stoul(argv[4]) : 3000;
   PROPER = argc > 5 && std::string(argv[5]) == "proper";
+  if (argc > 6) BRUTE = std::stoul(argv[6]);
   size_t na = A0.size() / W, nb = B0.size() / W;
   std::vector<double> fa(N_BITS), fb(N_BITS);
   for (size_t i = 0; i < na; ++i) for (int q = 0; q < N_BITS; ++q) fa[q] += test(&A0[i * W], q);
