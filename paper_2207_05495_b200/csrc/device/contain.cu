@@ -128,28 +128,29 @@ ContainIndex build_index(Context& c, const DList& a) {
 }
 
 // ---------------------------------------------------------------------------
-// Warp-cooperative work-pool traversal.
+// Query kernel: lane-owned queries + intra-warp work stealing.
 //
 // Per-query walks are heavy-tailed (n=300: mean ~1e3 node visits, p99 ~8e3,
-// max ~6e4), so one-thread-per-query leaves warps waiting on their slowest
-// lane and a small batch (the meet check: ~2e4 queries) runs for the serial
-// latency of its longest walk.  Here every warp owns a LIFO pool of tasks
-// (query j, node, first key of the node's range, next bit d, |y|) in shared
-// memory.  Each round the lanes pop up to 32 tasks from any mix of queries,
-// evaluate them and push the admissible children with ballot-compacted
-// stores; when fewer than 32 tasks remain the warp pulls new queries from a
-// global counter (persistent grid).  Loads are staged to keep the L1/TEX
-// pipe (the measured bottleneck) light: the node record first, then only the
-// words of y and of the node's first key that the prefix check touches.
-// Small ranges are scanned cooperatively: all (range, key) pairs of the warp
-// are flattened over the lanes (consecutive keys → coalesced rows) with the
-// owner's y broadcast by shuffles.
-constexpr int kPoolWarps = 6;
-constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 480;   // tasks per warp (static smem <= 48 KB per block)
-constexpr int kPoolBrute = 16;  // ranges of <= this many keys are scanned
+// max ~6e4).  Each lane owns one query at a time (its row y lives in
+// registers) and a private deque of pending subtrees in shared memory
+// (entry k of lane l at [k][l]: bank-conflict free).  A lane whose deque
+// empties takes the next query from a global counter (warp-aggregated
+// atomics; persistent grid), so lanes never wait on each other while queries
+// remain.  Once they run out, idle lanes steal the OLDEST pending subtree
+// (the largest) from busy lanes of their warp, receiving the victim's query
+// row by shuffles — a giant walk is spread over 32 lanes instead of
+// finishing serially.  Ranges of <= kLaneBrute keys are scanned
+// cooperatively: all (range, key) pairs of the warp are flattened over the
+// lanes (consecutive keys → coalesced rows), the owner's y by shuffles.
+// Per node visit a lane loads the 16-B node and the node's first key row,
+// concurrently (the task carries the range start).
+constexpr int kLaneWarps = 4;
+constexpr int kLaneThreads = kLaneWarps * 32;
+constexpr int kLaneCap = 40;    // deque entries per lane
+constexpr int kLaneBrute = 16;  // ranges of <= this many keys are scanned
 constexpr int kHitSlots = 64;   // per-warp table of recently hit queries (MARK mode)
 constexpr u32 kNone = 0xFFFFFFFFu;
+constexpr size_t kLaneSmemPerWarp = static_cast<size_t>(kLaneCap) * 32 * (4 + 4 + 2);
 
 template <int W>
 __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (&y)[W]) {
@@ -160,162 +161,157 @@ __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (
 }
 
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
+__global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
     const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
     u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u32 Nb,
     uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
-  __shared__ u32 s_q[kPoolWarps][kPoolCap];
-  __shared__ u32 s_n[kPoolWarps][kPoolCap];
-  __shared__ u32 s_f[kPoolWarps][kPoolCap];
-  __shared__ u32 s_dc[kPoolWarps][kPoolCap];  // d | |y| << 16
-  __shared__ u32 s_hit[kPoolWarps][kHitSlots];
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ u32 s_hit[kLaneWarps][kHitSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
-  u32* sq = s_q[wid];
-  u32* sn = s_n[wid];
-  u32* sf = s_f[wid];
-  u32* sdc = s_dc[wid];
+  u32* sid = reinterpret_cast<u32*>(dyn + wid * kLaneSmemPerWarp);
+  u32* sfirst = sid + kLaneCap * 32;
+  uint16_t* sd = reinterpret_cast<uint16_t*>(sfirst + kLaneCap * 32);
   u32* shit = s_hit[wid];
   for (int i = lane; i < kHitSlots; i += 32) shit[i] = kNone;
   __syncwarp();
   const u32 root_id = Na == 1 ? kLeafBit : 0u;
-  int sp = 0;
-  bool more = true;
+  int top = 0, bot = 0;
+  u32 j = kNone, cy = 0;
+  u64 y[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) y[w] = 0;
+  bool more = true;  // warp-uniform: global queries may remain
   while (true) {
     if (EXIST && *reinterpret_cast<volatile int*>(found)) break;
-    if (sp < 32 && more) {  // refill with fresh queries
+    if (!EXIST && j != kNone && shit[j % kHitSlots] == j) top = bot = 0;  // query already marked
+    // ---- 1. empty lanes take fresh queries
+    if (top == bot) {
+      top = bot = 0;
+      j = kNone;
+    }
+    const unsigned need = __ballot_sync(FULL, top == bot);
+    if (need && more) {
+      const int leader = __ffs(need) - 1;
       u32 base = 0;
-      if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
-      base = __shfl_sync(FULL, base, 0);
-      const u32 got = base >= Nb ? 0 : min(static_cast<u32>(32 - sp), Nb - base);
-      if (base + (32 - sp) >= Nb) more = false;
-      const u32 j = base + lane;
-      bool push = static_cast<u32>(lane) < got;
-      const u32 cy = push ? Bcard[j] : 0;
-      if (PROPER && cy == 0) push = false;
-      const unsigned m = __ballot_sync(FULL, push);
-      if (push) {
-        const int pos = sp + __popc(m & lt);
-        sq[pos] = j;
-        sn[pos] = root_id;
-        sf[pos] = 0;
-        sdc[pos] = cy << 16;
+      if (lane == leader) base = atomicAdd(next_query, static_cast<u32>(__popc(need)));
+      base = __shfl_sync(FULL, base, leader);
+      if (base + __popc(need) >= Nb) more = false;
+      if ((need >> lane) & 1) {
+        const u32 q = base + __popc(need & lt);
+        if (q < Nb) {
+          cy = Bcard[q];
+          if (!(PROPER && cy == 0)) {
+            j = q;
+#pragma unroll
+            for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(q) * W + w];
+            sid[lane] = root_id;
+            sfirst[lane] = 0;
+            sd[lane] = 0;
+            top = 1;
+          }
+        }
       }
-      sp += __popc(m);
-      __syncwarp();
     }
-    if (sp == 0) {
-      if (!more) break;
-      continue;
+    // ---- 2. no queries left: idle lanes steal the oldest subtree of busy lanes
+    if (!more) {
+      const bool idle = top == bot;
+      const unsigned idlem = __ballot_sync(FULL, idle);
+      const unsigned donm = __ballot_sync(FULL, top - bot >= 2);
+      if (idlem && donm) {
+        const int npair = min(__popc(idlem), __popc(donm));
+        const int ri = __popc(idlem & lt), rd = __popc(donm & lt);
+        int src = lane;
+        if (idle && ri < npair) src = __fns(donm, 0, ri + 1);
+        const int sbot = __shfl_sync(FULL, bot, src);
+        const u32 sj = __shfl_sync(FULL, j, src);
+        const u32 scy = __shfl_sync(FULL, cy, src);
+        u64 sy[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) sy[w] = __shfl_sync(FULL, y[w], src);
+        if (src != lane) {
+          sid[lane] = sid[sbot * 32 + src];
+          sfirst[lane] = sfirst[sbot * 32 + src];
+          sd[lane] = sd[sbot * 32 + src];
+          top = 1;
+          bot = 0;
+          j = sj;
+          cy = scy;
+#pragma unroll
+          for (int w = 0; w < W; ++w) y[w] = sy[w];
+        }
+        __syncwarp();
+        if (((donm >> lane) & 1) && rd < npair) ++bot;
+      }
     }
-    const int take = sp < 32 ? sp : 32;
-    const bool have = lane < take;
-    u32 j = 0, id = 0, first = 0, dc = 0;
-    if (have) {
-      const int pos = sp - 1 - lane;
-      j = sq[pos];
-      id = sn[pos];
-      first = sf[pos];
-      dc = sdc[pos];
-    }
-    sp -= take;
-    __syncwarp();
-    const int d = static_cast<int>(dc & 0xFFFF);
-    const u32 cy = dc >> 16;
-    const u32 limit = PROPER ? cy - 1 : cy;
-    bool alive = have && !(!EXIST && shit[j % kHitSlots] == j);
-    const bool is_leaf = (id & kLeafBit) != 0;
+    if (!more && __ballot_sync(FULL, top != bot) == 0) break;
 
-    // ---- stage 1: node record (internal) or key cardinality (leaf)
+    // ---- 3. pop one task per lane and evaluate it
+    const bool have = top != bot;
+    u32 id = 0, first = 0;
+    int d = 0;
+    if (have) {
+      --top;
+      id = sid[top * 32 + lane];
+      first = sfirst[top * 32 + lane];
+      d = sd[top * 32 + lane];
+    }
+    const u32 limit = PROPER ? cy - 1 : cy;
+    const bool is_leaf = (id & kLeafBit) != 0;
     Node nd{};
     u32 kcard = 0;
-    if (alive) {
+    u64 xf[W];
+    if (have) {
       if (is_leaf) kcard = Acard[first];
       else nd = nodes[id];
-    }
-    bool brute = false, check = false;
-    int L = 0;
-    if (alive) {
-      if (is_leaf) {
-        alive = kcard <= limit;
-      } else if (nd.minc > limit) {
-        alive = false;
-      } else if (nd.last - nd.first < kPoolBrute) {
-        brute = true;
-      } else {
-        check = true;
-        L = nd.lcp;
-      }
-    }
-    // ---- stage 2: only the row words that are needed
-    const bool full_y = alive && (is_leaf || brute);
-    const int ylo = d >> 6, yhi = L >> 6, xhi = (L - 1) >> 6;
-    u64 y[W], xf[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      y[w] = (full_y || (check && w >= ylo && w <= yhi)) ? B[static_cast<u64>(j) * W + w] : 0;
-      xf[w] = ((alive && is_leaf) || (check && L > d && w >= ylo && w <= xhi))
-                  ? A[static_cast<u64>(first) * W + w]
-                  : 0;
-    }
-
-    bool hit = false;
-    u32 hit_a = 0;
-    u32 c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
-    if (alive && is_leaf && is_subset<W>(xf, y)) {
-      hit = true;
-      hit_a = first;
-    }
-    if (brute) {
-      bf = nd.first;
-      bl = nd.last;
-    }
-    if (check) {
-      u64 bad = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-      if (!bad) {
-        c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-        f0 = nd.first;
-        if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
-          c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-          f1 = nd.split + 1;
-        }
-        bf = nd.first;
-        bl = nd.last;
-      }
-    }
-
-    // ---- push children (LIFO; left on top)
-    const u32 cdc = (cy << 16) | static_cast<u32>(L + 1);
-    const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
-    const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
-    const int n0 = __popc(m0), n1 = __popc(m1);
-    if (sp + n0 + n1 > kPoolCap) {
-      if (c0 != kNone) {  // pool full: scan the opened range instead
-        brute = true;
-#pragma unroll
-        for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
-      }
+      for (int w = 0; w < W; ++w) xf[w] = A[static_cast<u64>(first) * W + w];
     } else {
-      if (c1 != kNone) {
-        const int pos = sp + __popc(m1 & lt);
-        sq[pos] = j;
-        sn[pos] = c1;
-        sf[pos] = f1;
-        sdc[pos] = cdc;
+#pragma unroll
+      for (int w = 0; w < W; ++w) xf[w] = 0;
+    }
+    bool hit = false, brute = false;
+    u32 hit_a = 0, bf = 0, bl = 0;
+    if (have) {
+      if (is_leaf) {
+        if (kcard <= limit && is_subset<W>(xf, y)) {
+          hit = true;
+          hit_a = first;
+        }
+      } else if (nd.minc <= limit) {
+        if (nd.last - nd.first < kLaneBrute) {
+          brute = true;
+          bf = nd.first;
+          bl = nd.last;
+        } else {
+          const int L = nd.lcp;
+          u64 bad = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+          if (!bad) {
+            if (top + 2 > kLaneCap) {  // deque full: scan the opened range instead
+              brute = true;
+              bf = nd.first;
+              bl = nd.last;
+            } else {
+              const uint16_t dn = static_cast<uint16_t>(L + 1);
+              if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
+                sid[top * 32 + lane] = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+                sfirst[top * 32 + lane] = nd.split + 1;
+                sd[top * 32 + lane] = dn;
+                ++top;
+              }
+              sid[top * 32 + lane] = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+              sfirst[top * 32 + lane] = nd.first;
+              sd[top * 32 + lane] = dn;
+              ++top;
+            }
+          }
+        }
       }
-      if (c0 != kNone) {
-        const int pos = sp + n1 + __popc(m0 & lt);
-        sq[pos] = j;
-        sn[pos] = c0;
-        sf[pos] = f0;
-        sdc[pos] = cdc;
-      }
-      sp += n0 + n1;
     }
 
-    // ---- cooperative scan of small ranges
+    // ---- 4. cooperative scan of small ranges
     const u32 cnt = brute ? bl - bf + 1 : 0;
     u32 incl = cnt;
 #pragma unroll
@@ -381,22 +377,21 @@ static void launch_query(Context& c, const DList& a, const ContainIndex& ia, con
   if (a.empty()) return;
   u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..3)
   SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    int dev = 0;
-    SW_CUDA(cudaGetDevice(&dev));
-    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SW_DISPATCH_W(c.W(), {
-      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
-    });
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
+  constexpr size_t smem = kLaneWarps * kLaneSmemPerWarp;
+  int sms = 0, blocks_per_sm = 0, dev = 0;
+  SW_CUDA(cudaGetDevice(&dev));
+  SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SW_DISPATCH_W(c.W(), {
+    auto kern = contain_lane_kernel<W, PROPER, EXIST>;
+    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kLaneThreads, smem));
+  });
+  if (blocks_per_sm < 1) blocks_per_sm = 1;
+  const u64 want_blocks = (Nb + kLaneThreads - 1) / kLaneThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
   SW_DISPATCH_W(c.W(), {
-    contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
+    contain_lane_kernel<W, PROPER, EXIST><<<grid, kLaneThreads, smem, s>>>(
         a.words, a.cards, static_cast<const Node*>(ia.nodes), static_cast<u32>(a.size()), b.words,
         b.cards, static_cast<u32>(Nb), keep, found, wit, counter);
   });
