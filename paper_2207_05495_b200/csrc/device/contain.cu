@@ -4,19 +4,20 @@
 //
 // The reference splits a lex-sorted A on bit d by binary search and
 // partitions B in place, recursively — inherently sequential.  Here the
-// lex-sorted unique A becomes an explicit binary radix (Patricia) tree built
-// in parallel (Karras, HPG 2012: internal node i is found from the longest
-// common prefixes of neighbouring keys by binary search, no inter-thread
-// communication), each node annotated with its subtree's min cardinality.
-// A query y walks the tree depth-first:
+// lex-sorted unique A is turned into an explicit binary radix (Patricia) tree
+// in parallel (Karras, HPG 2012: node i of N-1 internal nodes is found from
+// longest-common-prefix lengths of neighbouring keys by binary search, no
+// inter-thread communication), each node annotated with its subtree's
+// minimum cardinality.  Every query set y is then handled by one thread that
+// walks the tree depth-first:
 //   * a node's keys agree on bits < lcp; bits [d, lcp) of that common prefix
 //     must lie in y (else the subtree is dead);
 //   * at the split bit L the 0-child is always admissible, the 1-child only if
 //     y has state L (exactly the reference's "ones side recurses with B_1");
 //   * subtrees whose min cardinality exceeds |y| (|y|-1 for proper) are cut —
 //     the reference's per-pair card filter lifted to whole subtrees;
-//   * ranges of <= kPoolBrute keys are scanned (warp-cooperatively).
-// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} does not depend on the
+//   * ranges of <= kBrute keys are scanned linearly (contiguous rows).
+// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} is independent of
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
 
@@ -33,8 +34,9 @@ struct __align__(16) Node {
   uint16_t minc;    // min cardinality in the range
 };
 
-
 constexpr u32 kLeafBit = 0x80000000u;
+constexpr int kBrute = 12;
+constexpr int kStack = 64;
 
 template <int W>
 __device__ __forceinline__ int key_delta(const u64* __restrict__ A, long long N, long long i,
@@ -127,31 +129,6 @@ ContainIndex build_index(Context& c, const DList& a) {
   return ix;
 }
 
-// ---------------------------------------------------------------------------
-// Query kernel: lane-owned queries + intra-warp work stealing.
-//
-// Per-query walks are heavy-tailed (n=300: mean ~1e3 node visits, p99 ~8e3,
-// max ~6e4).  Each lane owns one query at a time (its row y lives in
-// registers) and a private deque of pending subtrees in shared memory
-// (entry k of lane l at [k][l]: bank-conflict free).  A lane whose deque
-// empties takes the next query from a global counter (warp-aggregated
-// atomics; persistent grid), so lanes never wait on each other while queries
-// remain.  Once they run out, idle lanes steal the OLDEST pending subtree
-// (the largest) from busy lanes of their warp, receiving the victim's query
-// row by shuffles — a giant walk is spread over 32 lanes instead of
-// finishing serially.  Ranges of <= kLaneBrute keys are scanned
-// cooperatively: all (range, key) pairs of the warp are flattened over the
-// lanes (consecutive keys → coalesced rows), the owner's y by shuffles.
-// Per node visit a lane loads the 16-B node and the node's first key row,
-// concurrently (the task carries the range start).
-constexpr int kLaneWarps = 4;
-constexpr int kLaneThreads = kLaneWarps * 32;
-constexpr int kLaneCap = 40;    // deque entries per lane
-constexpr int kLaneBrute = 16;  // ranges of <= this many keys are scanned
-constexpr int kHitSlots = 64;   // per-warp table of recently hit queries (MARK mode)
-constexpr u32 kNone = 0xFFFFFFFFu;
-constexpr size_t kLaneSmemPerWarp = static_cast<size_t>(kLaneCap) * 32 * (4 + 4 + 2);
-
 template <int W>
 __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (&y)[W]) {
   u64 acc = 0;
@@ -160,126 +137,207 @@ __device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (
   return acc == 0;
 }
 
+// One thread per query y.  EXIST: stop everything at the first hit (meet
+// check / DFS trie query); otherwise write keep[j] = !hit.
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
+__global__ void __launch_bounds__(128) contain_query_kernel(
+    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
+    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u64 Nb,
+    uint8_t* __restrict__ keep, int* found, unsigned long long* wit) {
+  const u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  if (j >= Nb) return;
+  if (EXIST && *reinterpret_cast<volatile int*>(found)) return;
+  u64 y[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) y[w] = B[j * W + w];
+  const u32 cy = Bcard[j];
+  bool hit = false;
+  u32 hit_a = 0;
+  if (Na > 0 && !(PROPER && cy == 0)) {
+    const u32 limit = PROPER ? cy - 1 : cy;
+    u32 st_id[kStack];
+    uint16_t st_d[kStack];
+    int sp = 0;
+    st_id[sp] = Na == 1 ? kLeafBit : 0u;
+    st_d[sp++] = 0;
+    u32 iter = 0;
+    while (sp > 0 && !hit) {
+      if (EXIST && ((++iter & 63) == 0) && *reinterpret_cast<volatile int*>(found)) break;
+      --sp;
+      const u32 id = st_id[sp];
+      const int d = st_d[sp];
+      if (id & kLeafBit) {
+        const u32 x = id & ~kLeafBit;
+        if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+          hit = true;
+          hit_a = x;
+        }
+        continue;
+      }
+      const Node nd = nodes[id];
+      if (nd.minc > limit) continue;
+      if (nd.last - nd.first < kBrute) {
+        for (u32 x = nd.first; x <= nd.last; ++x)
+          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+            hit = true;
+            hit_a = x;
+            break;
+          }
+        continue;
+      }
+      const int L = nd.lcp;
+      // Bits [d, L) are common to the whole range: they must lie in y.
+      const u64* xf = A + static_cast<u64>(nd.first) * W;
+      u64 bad = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+      if (bad) continue;
+      const u32 left = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+      const u32 right = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+      const bool y_has_L = (y[L >> 6] >> (63 - (L & 63))) & 1;
+      if (sp + 2 > kStack) {
+        // Stack exhausted (very deep tree): finish this subtree linearly.
+        for (u32 x = nd.first; x <= nd.last; ++x)
+          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
+            hit = true;
+            hit_a = x;
+            break;
+          }
+        continue;
+      }
+      if (y_has_L) {
+        st_id[sp] = right;
+        st_d[sp++] = static_cast<uint16_t>(L + 1);
+      }
+      st_id[sp] = left;
+      st_d[sp++] = static_cast<uint16_t>(L + 1);
+    }
+  }
+  if (EXIST) {
+    if (hit && atomicCAS(found, 0, 1) == 0) {
+      wit[0] = hit_a;
+      wit[1] = j;
+    }
+  } else {
+    keep[j] = hit ? 0 : 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative work-pool traversal (the production query kernel).
+//
+// Per-query traversal lengths are heavy-tailed (n=300: mean ~1e3 node visits,
+// p99 ~8e3, max ~6e4), so one-thread-per-query leaves warps waiting on their
+// slowest lane and a small query batch (the meet check: ~2e4 queries) runs
+// for the serial latency of its longest walk.  Here every warp owns a LIFO
+// pool of (query, node, depth) tasks in shared memory.  Each round the 32
+// lanes pop 32 tasks — from any mix of queries — test them, and push the
+// admissible children back with ballot-compacted stores; when the pool holds
+// fewer than 32 tasks the warp pulls new queries from a global counter.
+// Long queries are thereby spread over all lanes, short ones pack densely,
+// and the grid is persistent (a fixed number of CTAs per SM).
+constexpr int kPoolWarps = 6;
+constexpr int kPoolThreads = kPoolWarps * 32;
+constexpr int kPoolCap = 512;  // tasks per warp
+constexpr int kPoolBrute = 16; // ranges of <= this many keys are scanned cooperatively
+constexpr u32 kNone = 0xFFFFFFFFu;
+
+// A task is (query j, tree node id | kLeafBit, first key of the node's range,
+// next bit to check).  Carrying `first` lets the node record, the node's
+// first key (prefix check), the query row and the flags load concurrently:
+// one memory round trip per task.
+template <int W, bool PROPER, bool EXIST>
+__global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
     u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u32 Nb,
     uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ u32 s_hit[kLaneWarps][kHitSlots];
+  __shared__ u32 s_q[kPoolWarps][kPoolCap];
+  __shared__ u32 s_n[kPoolWarps][kPoolCap];
+  __shared__ u32 s_f[kPoolWarps][kPoolCap];
+  __shared__ uint16_t s_d[kPoolWarps][kPoolCap];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
-  u32* sid = reinterpret_cast<u32*>(dyn + wid * kLaneSmemPerWarp);
-  u32* sfirst = sid + kLaneCap * 32;
-  uint16_t* sd = reinterpret_cast<uint16_t*>(sfirst + kLaneCap * 32);
-  u32* shit = s_hit[wid];
-  for (int i = lane; i < kHitSlots; i += 32) shit[i] = kNone;
-  __syncwarp();
+  u32* sq = s_q[wid];
+  u32* sn = s_n[wid];
+  u32* sf = s_f[wid];
+  uint16_t* sd = s_d[wid];
   const u32 root_id = Na == 1 ? kLeafBit : 0u;
-  int top = 0, bot = 0;
-  u32 j = kNone, cy = 0;
-  u64 y[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) y[w] = 0;
-  bool more = true;  // warp-uniform: global queries may remain
+  int sp = 0;
+  bool more = true;
   while (true) {
     if (EXIST && *reinterpret_cast<volatile int*>(found)) break;
-    if (!EXIST && j != kNone && shit[j % kHitSlots] == j) top = bot = 0;  // query already marked
-    // ---- 1. empty lanes take fresh queries
-    if (top == bot) {
-      top = bot = 0;
-      j = kNone;
-    }
-    const unsigned need = __ballot_sync(FULL, top == bot);
-    if (need && more) {
-      const int leader = __ffs(need) - 1;
+    if (sp < 32 && more) {  // refill with fresh queries
       u32 base = 0;
-      if (lane == leader) base = atomicAdd(next_query, static_cast<u32>(__popc(need)));
-      base = __shfl_sync(FULL, base, leader);
-      if (base + __popc(need) >= Nb) more = false;
-      if ((need >> lane) & 1) {
-        const u32 q = base + __popc(need & lt);
-        if (q < Nb) {
-          cy = Bcard[q];
-          if (!(PROPER && cy == 0)) {
-            j = q;
-#pragma unroll
-            for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(q) * W + w];
-            sid[lane] = root_id;
-            sfirst[lane] = 0;
-            sd[lane] = 0;
-            top = 1;
-          }
-        }
+      if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
+      base = __shfl_sync(FULL, base, 0);
+      const u32 got = base >= Nb ? 0 : min(static_cast<u32>(32 - sp), Nb - base);
+      if (base + (32 - sp) >= Nb) more = false;
+      const u32 j = base + lane;
+      bool push = static_cast<u32>(lane) < got;
+      if (push && PROPER && Bcard[j] == 0) push = false;
+      const unsigned m = __ballot_sync(FULL, push);
+      if (push) {
+        const int pos = sp + __popc(m & lt);
+        sq[pos] = j;
+        sn[pos] = root_id;
+        sf[pos] = 0;
+        sd[pos] = 0;
       }
+      sp += __popc(m);
+      __syncwarp();
     }
-    // ---- 2. no queries left: idle lanes steal the oldest subtree of busy lanes
-    if (!more) {
-      const bool idle = top == bot;
-      const unsigned idlem = __ballot_sync(FULL, idle);
-      const unsigned donm = __ballot_sync(FULL, top - bot >= 2);
-      if (idlem && donm) {
-        const int npair = min(__popc(idlem), __popc(donm));
-        const int ri = __popc(idlem & lt), rd = __popc(donm & lt);
-        int src = lane;
-        if (idle && ri < npair) src = __fns(donm, 0, ri + 1);
-        const int sbot = __shfl_sync(FULL, bot, src);
-        const u32 sj = __shfl_sync(FULL, j, src);
-        const u32 scy = __shfl_sync(FULL, cy, src);
-        u64 sy[W];
-#pragma unroll
-        for (int w = 0; w < W; ++w) sy[w] = __shfl_sync(FULL, y[w], src);
-        if (src != lane) {
-          sid[lane] = sid[sbot * 32 + src];
-          sfirst[lane] = sfirst[sbot * 32 + src];
-          sd[lane] = sd[sbot * 32 + src];
-          top = 1;
-          bot = 0;
-          j = sj;
-          cy = scy;
-#pragma unroll
-          for (int w = 0; w < W; ++w) y[w] = sy[w];
-        }
-        __syncwarp();
-        if (((donm >> lane) & 1) && rd < npair) ++bot;
-      }
+    if (sp == 0) {
+      if (!more) break;
+      continue;
     }
-    if (!more && __ballot_sync(FULL, top != bot) == 0) break;
-
-    // ---- 3. pop one task per lane and evaluate it
-    const bool have = top != bot;
-    u32 id = 0, first = 0;
+    const int take = sp < 32 ? sp : 32;
+    bool have = lane < take;
+    u32 j = 0, id = 0, first = 0;
     int d = 0;
     if (have) {
-      --top;
-      id = sid[top * 32 + lane];
-      first = sfirst[top * 32 + lane];
-      d = sd[top * 32 + lane];
+      const int pos = sp - 1 - lane;
+      j = sq[pos];
+      id = sn[pos];
+      first = sf[pos];
+      d = sd[pos];
     }
-    const u32 limit = PROPER ? cy - 1 : cy;
-    const bool is_leaf = (id & kLeafBit) != 0;
+    sp -= take;
+    __syncwarp();
+
+    // ---- one concurrent round of loads
+    u64 y[W], xf[W];
+    u32 cy = 0, kcard = 0;
     Node nd{};
-    u32 kcard = 0;
-    u64 xf[W];
+    bool alive = have;
     if (have) {
-      if (is_leaf) kcard = Acard[first];
-      else nd = nodes[id];
+#pragma unroll
+      for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
 #pragma unroll
       for (int w = 0; w < W; ++w) xf[w] = A[static_cast<u64>(first) * W + w];
+      cy = Bcard[j];
+      if (id & kLeafBit) kcard = Acard[first];
+      else nd = nodes[id];
+      if (!EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) alive = false;
     } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) xf[w] = 0;
+      for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
     }
-    bool hit = false, brute = false;
-    u32 hit_a = 0, bf = 0, bl = 0;
-    if (have) {
-      if (is_leaf) {
+    const u32 limit = PROPER ? cy - 1 : cy;
+
+    // ---- evaluate the task
+    bool hit = false;
+    u32 hit_a = 0;
+    u32 c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
+    bool brute = false;
+    int dchild = 0;
+    if (alive) {
+      if (id & kLeafBit) {
         if (kcard <= limit && is_subset<W>(xf, y)) {
           hit = true;
           hit_a = first;
         }
       } else if (nd.minc <= limit) {
-        if (nd.last - nd.first < kLaneBrute) {
+        if (nd.last - nd.first < kPoolBrute) {
           brute = true;
           bf = nd.first;
           bl = nd.last;
@@ -289,29 +347,48 @@ __global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
 #pragma unroll
           for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
           if (!bad) {
-            if (top + 2 > kLaneCap) {  // deque full: scan the opened range instead
-              brute = true;
-              bf = nd.first;
-              bl = nd.last;
-            } else {
-              const uint16_t dn = static_cast<uint16_t>(L + 1);
-              if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
-                sid[top * 32 + lane] = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-                sfirst[top * 32 + lane] = nd.split + 1;
-                sd[top * 32 + lane] = dn;
-                ++top;
-              }
-              sid[top * 32 + lane] = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-              sfirst[top * 32 + lane] = nd.first;
-              sd[top * 32 + lane] = dn;
-              ++top;
+            const bool lleaf = nd.split == nd.first, rleaf = nd.split + 1 == nd.last;
+            c0 = lleaf ? (kLeafBit | nd.first) : nd.split;
+            f0 = nd.first;
+            if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
+              c1 = rleaf ? (kLeafBit | nd.last) : nd.split + 1;
+              f1 = nd.split + 1;
             }
+            dchild = L + 1;
+            bf = nd.first;
+            bl = nd.last;
           }
         }
       }
     }
 
-    // ---- 4. cooperative scan of small ranges
+    // ---- push children (LIFO; left on top)
+    const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
+    const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
+    const int n0 = __popc(m0), n1 = __popc(m1);
+    if (sp + n0 + n1 > kPoolCap) {
+      if (c0 != kNone) brute = true;  // pool full: scan the opened range instead
+    } else {
+      if (c1 != kNone) {
+        const int pos = sp + __popc(m1 & lt);
+        sq[pos] = j;
+        sn[pos] = c1;
+        sf[pos] = f1;
+        sd[pos] = static_cast<uint16_t>(dchild);
+      }
+      if (c0 != kNone) {
+        const int pos = sp + n1 + __popc(m0 & lt);
+        sq[pos] = j;
+        sn[pos] = c0;
+        sf[pos] = f0;
+        sd[pos] = static_cast<uint16_t>(dchild);
+      }
+      sp += n0 + n1;
+    }
+    __syncwarp();
+
+    // ---- cooperative scan of small ranges: all (range, key) pairs of the warp
+    // are flattened and spread over the lanes, 32 independent key tests per pass.
     const u32 cnt = brute ? bl - bf + 1 : 0;
     u32 incl = cnt;
 #pragma unroll
@@ -339,7 +416,12 @@ __global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
       for (int w = 0; w < W; ++w) oy[w] = __shfl_sync(FULL, y[w], owner);
       if (t < total) {
         const u32 key = o_bf + (t - o_excl);
-        if (Acard[key] <= o_lim && is_subset<W>(A + static_cast<u64>(key) * W, oy)) {
+        // card and row issued together: one memory round trip per pass
+        const u32 kc = Acard[key];
+        u64 kr[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) kr[w] = A[static_cast<u64>(key) * W + w];
+        if (kc <= o_lim && is_subset<W>(kr, oy)) {
           if (EXIST) {
             if (atomicCAS(found, 0, 1) == 0) {
               wit[0] = key;
@@ -347,7 +429,6 @@ __global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
             }
           } else {
             keep[o_j] = 0;
-            shit[o_j % kHitSlots] = o_j;
           }
         }
       }
@@ -360,7 +441,6 @@ __global__ void __launch_bounds__(kLaneThreads) contain_lane_kernel(
         }
       } else {
         keep[j] = 0;
-        shit[j % kHitSlots] = j;
       }
     }
     __syncwarp();
@@ -377,21 +457,22 @@ static void launch_query(Context& c, const DList& a, const ContainIndex& ia, con
   if (a.empty()) return;
   u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..3)
   SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-  constexpr size_t smem = kLaneWarps * kLaneSmemPerWarp;
-  int sms = 0, blocks_per_sm = 0, dev = 0;
-  SW_CUDA(cudaGetDevice(&dev));
-  SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  SW_DISPATCH_W(c.W(), {
-    auto kern = contain_lane_kernel<W, PROPER, EXIST>;
-    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kLaneThreads, smem));
-  });
-  if (blocks_per_sm < 1) blocks_per_sm = 1;
-  const u64 want_blocks = (Nb + kLaneThreads - 1) / kLaneThreads;
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    SW_CUDA(cudaGetDevice(&dev));
+    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SW_DISPATCH_W(c.W(), {
+      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
+    });
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
   SW_DISPATCH_W(c.W(), {
-    contain_lane_kernel<W, PROPER, EXIST><<<grid, kLaneThreads, smem, s>>>(
+    contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         a.words, a.cards, static_cast<const Node*>(ia.nodes), static_cast<u32>(a.size()), b.words,
         b.cards, static_cast<u32>(Nb), keep, found, wit, counter);
   });
