@@ -170,6 +170,17 @@ int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count, const uint
 int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
                        const uint64_t* b_words, size_t b_count, int32_t* met);
 /* Node count of the reference StaticTrie over a duplicate-free list. */
+/* ---- cost model (cost_model.hpp:67-250), host-side doubles ---- */
+double sw_exp_mark(double a_size, double b_size, double a_density, double b_density);
+/* stats[18] = {k, r, R, then per side (BFS, IBFS): list_size, list_density,
+ * hist_size, hist_density, r_dupl, r_self, r_hist}; flags[7] = {bfs.hist_dropped,
+ * bfs.step_feasible, bfs.nh_feasible, ibfs.hist_dropped, ibfs.step_feasible,
+ * ibfs.nh_feasible, dfs_feasible}; tuning[4] = {set_cost, dfs_set_weight,
+ * dfs_check_weight, reduction_of_reduction (<= 0: 1/k)}.  Writes step[5],
+ * pred[5], feasible[5] and the selected StepKind. */
+int sw_step_costs(const double* stats, const int32_t* flags, const double* tuning, double* step,
+                  double* pred, int32_t* feasible, int32_t* selected);
+
 int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t min_leaf,
                        uint64_t* nodes);
 

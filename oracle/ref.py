@@ -124,8 +124,22 @@ def lib():
                                       C.POINTER(RefResult), _u32p, C.c_size_t, C.c_char_p]
         L.ref_solve_instrumented.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(RefOptions),
                                              C.POINTER(RefResult), C.c_char_p, C.c_char_p]
+        _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        _ip = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+        L.ref_step_costs.argtypes = [_dp, _ip, _dp, _dp, _dp, _ip, C.POINTER(C.c_int32)]
         _lib = L
     return _lib
+
+
+def step_costs(stats, flags, tuning):
+    st = np.ascontiguousarray(stats, np.float64)
+    fl = np.ascontiguousarray(flags, np.int32)
+    tu = np.ascontiguousarray(tuning, np.float64)
+    step, pred = np.zeros(5), np.zeros(5)
+    feas = np.zeros(5, np.int32)
+    sel = C.c_int32()
+    lib().ref_step_costs(st, fl, tu, step, pred, feas, C.byref(sel))
+    return step, pred, feas, sel.value
 
 
 # ----------------------------------------------------------------- automata

@@ -99,6 +99,49 @@ REF_API int64_t ref_power_set_oracle(uint32_t n, uint32_t k, const uint32_t* del
     return -2;
   }
 }
+// compute_step_costs + select_step (cost_model.hpp:187-250) on a flattened
+// SearchStats; same layout as sw_step_costs in include/synchro_b200.h.
+REF_API int ref_step_costs(const double* st, const int32_t* fl, const double* tu, double* step,
+                           double* pred, int32_t* feasible, int32_t* selected) {
+  SearchStats s;
+  s.k = st[0];
+  s.r = st[1];
+  s.R = st[2];
+  SideStats* sides[2] = {&s.bfs, &s.ibfs};
+  for (int i = 0; i < 2; ++i) {
+    const double* p = st + 3 + 7 * i;
+    SideStats& x = *sides[i];
+    x.list_size = p[0];
+    x.list_density = p[1];
+    x.hist_size = p[2];
+    x.hist_density = p[3];
+    x.r_dupl = p[4];
+    x.r_self = p[5];
+    x.r_hist = p[6];
+    x.hist_dropped = fl[3 * i] != 0;
+    x.step_feasible = fl[3 * i + 1] != 0;
+    x.nh_feasible = fl[3 * i + 2] != 0;
+  }
+  s.dfs_feasible = fl[6] != 0;
+  TuningParams t;
+  t.set_cost = tu[0];
+  t.dfs_set_cost_weight = tu[1];
+  t.dfs_check_cost_weight = tu[2];
+  if (tu[3] > 0) t.dfs_reduction_of_reduction = tu[3];
+  const StepCosts c = compute_step_costs(s, t);
+  for (int i = 0; i < 5; ++i) {
+    step[i] = c.step[i];
+    pred[i] = c.pred[i];
+    feasible[i] = c.feasible[i] ? 1 : 0;
+  }
+  try {
+    *selected = static_cast<int32_t>(select_step(c));
+  } catch (const OutOfMemoryError&) {
+    *selected = -1;
+  }
+  return 0;
+}
+
 REF_API double ref_exp_mark(double as, double bs, double ad, double bd) {
   return exp_mark(as, bs, ad, bd);
 }

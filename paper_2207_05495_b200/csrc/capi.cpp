@@ -414,6 +414,44 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
   });
 }
 
+SW_EXPORT double sw_exp_mark(double as, double bs, double ad, double bd) {
+  return exp_mark(as, bs, ad, bd);
+}
+
+SW_EXPORT int sw_step_costs(const double* st, const int32_t* fl, const double* tu, double* step,
+                            double* pred, int32_t* feasible, int32_t* selected) {
+  return guarded([&] {
+    SearchStats s;
+    s.k = st[0];
+    s.r = st[1];
+    s.R = st[2];
+    SideStats* sides[2] = {&s.bfs, &s.ibfs};
+    for (int i = 0; i < 2; ++i) {
+      const double* p = st + 3 + 7 * i;
+      *sides[i] = SideStats{p[0], p[1], p[2], p[3], p[4], p[5], p[6],
+                            fl[3 * i] != 0, fl[3 * i + 1] != 0, fl[3 * i + 2] != 0};
+    }
+    s.dfs_feasible = fl[6] != 0;
+    TuningParams t;
+    t.set_cost = tu[0];
+    t.dfs_set_cost_weight = tu[1];
+    t.dfs_check_cost_weight = tu[2];
+    if (tu[3] > 0) t.dfs_reduction_of_reduction = tu[3];
+    const StepCosts c = compute_step_costs(s, t);
+    for (int i = 0; i < 5; ++i) {
+      step[i] = c.step[i];
+      pred[i] = c.pred[i];
+      feasible[i] = c.feasible[i] ? 1 : 0;
+    }
+    *selected = -1;
+    try {
+      *selected = static_cast<int32_t>(select_step(c));
+    } catch (const OutOfMemoryError&) {
+      *selected = -1;
+    }
+  });
+}
+
 SW_EXPORT int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t min_leaf,
                                  uint64_t* nodes) {
   return guarded([&] {

@@ -32,7 +32,8 @@ EXPORTED_SYMBOLS = [
     "sw_engine_step", "sw_engine_meet", "sw_engine_dfs", "sw_engine_stats_get",
     "sw_list_expand", "sw_list_lex_sort_dedupe", "sw_list_sort_card_desc_lex",
     "sw_list_dedupe_sorted", "sw_list_self_reduce_minimal", "sw_list_mark",
-    "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment",
+    "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
+    "sw_step_costs",
 ]
 
 
@@ -155,8 +156,30 @@ def load():
     L.sw_run_experiment.argtypes = [_u32p, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint64,
                                     C.c_char_p, C.c_double, C.c_uint64, C.c_uint32, C.c_int32,
                                     C.c_uint32, C.c_uint32, C.c_char_p]
+    L.sw_exp_mark.argtypes = [C.c_double] * 4
+    L.sw_exp_mark.restype = C.c_double
+    _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    _ip = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+    L.sw_step_costs.argtypes = [_dp, _ip, _dp, _dp, _dp, _ip, C.POINTER(C.c_int32)]
     _lib = L
     return L
+
+
+def exp_mark(a_size: float, b_size: float, a_density: float, b_density: float) -> float:
+    """ExpMark (cost_model.hpp:67-74)."""
+    return float(load().sw_exp_mark(a_size, b_size, a_density, b_density))
+
+
+def step_costs(stats, flags, tuning):
+    """compute_step_costs + select_step (cost_model.hpp:187-250); see sw_step_costs."""
+    st = np.ascontiguousarray(stats, np.float64)
+    fl = np.ascontiguousarray(flags, np.int32)
+    tu = np.ascontiguousarray(tuning, np.float64)
+    step, pred = np.zeros(5), np.zeros(5)
+    feas = np.zeros(5, np.int32)
+    sel = C.c_int32()
+    _check(load().sw_step_costs(st, fl, tu, step, pred, feas, C.byref(sel)))
+    return step, pred, feas, sel.value
 
 
 def _check(rc: int) -> None:

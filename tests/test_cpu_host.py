@@ -1,0 +1,231 @@
+"""CPU-only tests (no GPU needed): the C-ABI library loads and exports every
+symbol include/synchro_b200.h declares; the host-side control plane (generators,
+text format, synchronizability, power-set oracle, Eppstein, the cost model)
+matches the reference bit-exactly; the CLI keeps the reference's formats and
+exit codes; the golden fixtures are self-consistent with the SPEC's KATs."""
+import json
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2207_05495_b200 import native as sw
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+CLI = sw.CLI_PATH
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "synchro_b200.h")).read()
+    return sorted(set(re.findall(r"\b(sw_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = sw.load()
+    declared = header_symbols()
+    assert len(declared) >= 30
+    missing = [s for s in declared if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(declared) == set(sw.EXPORTED_SYMBOLS)
+
+
+def test_version_and_device_count_without_gpu():
+    assert "sm_100a" in sw.version()
+    assert sw.device_count() >= 0
+
+
+@pytest.mark.parametrize("n,k,seed", [(1, 1, 0), (7, 2, 3), (100, 2, 0), (300, 2, 1), (570, 2, 0),
+                                      (200, 3, 0), (26, 25, 9)])
+def test_random_automaton_matches_reference(ref, n, k, seed):
+    assert np.array_equal(sw.random_automaton(n, k, seed).delta, ref.random_automaton(n, k, seed))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 20, 57])
+def test_cerny_matches_reference(ref, n):
+    assert np.array_equal(sw.cerny_automaton(n).delta, ref.cerny_automaton(n))
+
+
+def test_cerny_rejects_n1():
+    with pytest.raises(sw.SynchroError):
+        sw.cerny_automaton(1)
+
+
+def test_instance_seed_matches_reference(ref):
+    for base in (0, 12345, 2**63 + 7):
+        for n in (6, 100, 570):
+            for i in (0, 1, 999):
+                assert sw.instance_seed(base, n, i) == ref.instance_seed(base, n, i)
+
+
+def test_parse_automaton_format_and_errors():
+    a = sw.parse_automaton("# comment\n3 2\n1 2 # row 0\n2 0\n0 0\n")
+    assert (a.n, a.k) == (3, 2) and a.delta.tolist() == [1, 2, 2, 0, 0, 0]
+    for bad in ["", "2", "2 1\n0\n", "2 1\n0 5\n", "2 1\n0 -1\n", "2 1\n0 x\n", "0 1\n"]:
+        with pytest.raises(sw.SynchroError) as e:
+            sw.parse_automaton(bad)
+        assert e.value.code == 3
+
+
+def test_is_synchronizing_matches_reference(ref):
+    kats = json.load(open(os.path.join(GOLDEN, "powerset_kats.json")))
+    for kat in kats[::5]:
+        a = sw.random_automaton(kat["n"], kat["k"], kat["seed"])
+        assert sw.is_synchronizing(a) == (kat["oracle"] >= 0)
+    for n, k, s in [(100, 2, i) for i in range(20)] + [(300, 2, 0)]:
+        a = sw.random_automaton(n, k, s)
+        assert sw.is_synchronizing(a) == ref.is_synchronizing(n, k, a.delta)
+    assert not sw.is_synchronizing(sw.parse_automaton("3 2\n1 0\n2 1\n0 2\n"))
+
+
+def test_power_set_oracle_golden_kats():
+    kats = json.load(open(os.path.join(GOLDEN, "powerset_kats.json")))
+    assert len(kats) == 560
+    for kat in kats:
+        a = sw.random_automaton(kat["n"], kat["k"], kat["seed"])
+        if kat["oracle"] < 0:
+            with pytest.raises(sw.NotSynchronizingError):
+                sw.power_set_oracle(a)
+        else:
+            assert sw.power_set_oracle(a) == kat["oracle"]
+    assert sw.power_set_oracle(sw.cerny_automaton(4)) == 9
+
+
+def test_power_set_oracle_refuses_n21():
+    with pytest.raises(sw.SynchroError) as e:
+        sw.power_set_oracle(sw.random_automaton(21, 2, 0))
+    assert e.value.code == 5
+
+
+@pytest.mark.parametrize("n,k,seed", [(20, 2, 0), (50, 2, 1), (100, 2, 0), (300, 2, 0), (60, 3, 2),
+                                      (12, 2, 5)])
+def test_eppstein_matches_reference(ref, n, k, seed):
+    a = sw.random_automaton(n, k, seed)
+    if not ref.is_synchronizing(n, k, a.delta):
+        pytest.skip("not synchronizing")
+    bound, word = sw.heuristic(a, "eppstein")
+    rb, rw = ref.eppstein(n, k, a.delta)
+    assert (bound, word) == (rb, rw)
+    assert ref.is_reset_word(n, k, a.delta, word)
+
+
+def test_exp_mark_kat_and_bit_exact(ref):
+    assert sw.exp_mark(2, 2, 0.5, 0.5) == 21.0  # SPEC.md acceptance criterion
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        a, b = rng.uniform(0, 2e6, 2)
+        da, db = rng.uniform(-0.1, 1.1, 2)
+        assert sw.exp_mark(a, b, da, db) == ref.exp_mark(a, b, da, db)
+
+
+def test_step_costs_bit_exact_against_reference(ref):
+    rng = np.random.default_rng(1)
+    for i in range(3000):
+        stats = [rng.choice([2.0, 3.0]), float(rng.integers(1, 40)), float(rng.integers(20, 80))]
+        for _ in range(2):
+            stats += [float(rng.integers(0, 2_000_000)), rng.uniform(0, 1), float(rng.integers(0, 60000)),
+                      rng.uniform(0, 1), rng.uniform(0, 0.6), rng.uniform(0, 0.6), rng.uniform(0, 0.6)]
+        flags = rng.integers(0, 2, 7).tolist()
+        flags[1] = flags[2] = flags[4] = flags[5] = 1 if i % 3 else flags[1]
+        tuning = [512.0, 0.25, 0.25, 0.0] if i % 2 else [rng.uniform(1, 1000), rng.uniform(0, 1),
+                                                         rng.uniform(0, 1), rng.uniform(0, 1)]
+        g = sw.step_costs(stats, flags, tuning)
+        r = ref.step_costs(stats, flags, tuning)
+        assert np.array_equal(g[0], r[0]) and np.array_equal(g[1], r[1])
+        assert np.array_equal(g[2], r[2]) and g[3] == r[3]
+
+
+# ------------------------------------------------------------------- CLI
+def run_cli(*args, stdin=None):
+    return subprocess.run([CLI, *args], capture_output=True, text=True, input=stdin, timeout=120)
+
+
+def test_cli_gen_and_oracle():
+    r = run_cli("gen", "--gen", "cerny:4")
+    assert r.returncode == 0 and r.stdout == "4 2\n1 1\n2 1\n3 2\n0 3\n"
+    r = run_cli("oracle", "--gen", "cerny:4")
+    assert r.returncode == 0 and r.stdout == "threshold 9\n"
+    r = run_cli("oracle", "--input", "-", stdin="4 2\n1 1\n2 1\n3 2\n0 3\n")
+    assert r.stdout == "threshold 9\n"
+
+
+def test_cli_exit_codes():
+    assert run_cli("oracle", "--gen", "random:21,2,0").returncode == 5
+    assert run_cli("oracle", "--gen", "bogus:3").returncode == 3
+    assert run_cli("oracle", "--gen", "random:3,2").returncode == 3
+    assert run_cli("oracle", "--input", "/nonexistent").returncode == 3
+    assert run_cli("oracle", "--input", "-", stdin="3 2\n1 0\n2 1\n0 2\n").returncode == 2
+    assert run_cli("heuristic", "--input", "-", stdin="3 2\n1 0\n2 1\n0 2\n").returncode == 2
+    assert run_cli("exact").returncode != 0
+    assert run_cli("exact", "--gen", "cerny:4", "--schedule", "nope").returncode != 0
+    assert run_cli("nosuchcommand").returncode != 0
+
+
+def test_cli_heuristic_eppstein():
+    r = run_cli("heuristic", "--gen", "cerny:5", "--algorithm", "eppstein")
+    assert r.returncode == 0 and r.stdout.startswith("bound ") and "\nword " in r.stdout
+
+
+def test_cli_experiment_oracle_and_fit(tmp_path):
+    out = tmp_path / "e.csv"
+    r = run_cli("experiment", "--n", "8", "--n", "10", "--samples", "12", "--solver", "oracle",
+                "--deterministic", "--threads", "3", "-o", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().splitlines()
+    assert lines[0] == "n,k,seed,solver,threshold,status,time_s,peak_mem_bytes"
+    assert len(lines) == 25
+    kats = {(k["n"], k["seed"]): k["oracle"] for k in json.load(open(os.path.join(GOLDEN, "powerset_kats.json")))}
+    for row in lines[1:]:
+        n, k, seed, solver, thr, status, t, peak = row.split(",")
+        assert solver == "oracle" and t == "0.000000" and int(seed) == sw.instance_seed(0, int(n), lines.index(row) - 1 - (0 if n == "8" else 12))
+        assert status in ("ok", "nonsync")
+    r = run_cli("fit", "--input", str(out))
+    assert r.returncode == 0 and r.stdout.startswith("a ") and "\nc " in r.stdout
+
+
+def test_cli_experiment_sharding_partitions_rows(tmp_path):
+    full = tmp_path / "full.csv"
+    run_cli("experiment", "--n", "9", "--samples", "10", "--solver", "oracle", "--deterministic", "-o", str(full))
+    parts = []
+    for s in range(3):
+        p = tmp_path / f"s{s}.csv"
+        r = run_cli("experiment", "--n", "9", "--samples", "10", "--solver", "oracle", "--deterministic",
+                    "--shard-index", str(s), "--shard-count", "3", "-o", str(p))
+        assert r.returncode == 0
+        parts += p.read_text().splitlines()[1:]
+    assert sorted(parts) == sorted(full.read_text().splitlines()[1:])
+
+
+# -------------------------------------------------------- golden fixtures
+def test_golden_cerny_thresholds():
+    cases = json.load(open(os.path.join(GOLDEN, "solve_small.json")))
+    for c in cases:
+        if c["spec"].startswith("cerny:") and not c["options"]:
+            n = int(c["spec"].split(":")[1])
+            assert c["threshold"] == (n - 1) ** 2
+
+
+def test_golden_batch_mean_matches_spec():
+    b = json.load(open(os.path.join(GOLDEN, "batch_n100_k2.json")))
+    thr = [r[2] for r in b["rows"] if r[2] > 0]
+    assert len(b["rows"]) == 1000 and len(thr) == 999
+    mean = sum(thr) / len(thr)
+    assert abs(mean - 24.5) <= 0.1 * 24.5  # SPEC.md acceptance: within ±10% of 24.5
+    assert abs(mean - 24.3163) < 1e-3
+
+
+def test_golden_n300_matches_survey():
+    c = json.load(open(os.path.join(GOLDEN, "solve_random_300_2_0.json")))
+    assert c["threshold"] == 44 and c["expansions_phase1"] + c["expansions_dfs"] == 8505740
+    assert [lv["kept"] for lv in c["dfs_levels"]] == [34217, 68434, 131158, 162222, 318442, 636884,
+                                                      771763, 1543526]
+
+
+def test_reference_small_solve_reproduces_golden(ref, tmp_path):
+    cases = json.load(open(os.path.join(GOLDEN, "solve_small.json")))
+    for c in cases[:12]:
+        a = sw.from_spec(c["spec"])
+        s = ref.solve_exact(a.n, a.k, a.delta, trace_path=str(tmp_path / "t"), **c["options"])
+        assert s.threshold == c["threshold"] and s.trace == c["trace"]
