@@ -393,8 +393,8 @@ SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
       dev::lex_sort_dedupe(c, a);
       dev::complement(c, b);
     }
-    const dev::ContainIndex ix = dev::build_index(c, a);
-    const std::vector<uint8_t> k = dev::superset_keep(c, a, ix, b, mode == 1);
+    const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
+    const std::vector<uint8_t> k = dev::superset_keep(c, ix, b, mode == 1);
     std::memcpy(keep, k.data(), k.size());
   });
 }
@@ -409,8 +409,8 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
     dev::Context c(identity_aut(n));
     dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
-    const dev::ContainIndex ix = dev::build_index(c, a);
-    *met = dev::exists_subset(c, a, ix, b, nullptr) ? 1 : 0;
+    const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
+    *met = dev::exists_subset(c, ix, b, nullptr) ? 1 : 0;
   });
 }
 

@@ -4,20 +4,19 @@
 //
 // The reference splits a lex-sorted A on bit d by binary search and
 // partitions B in place, recursively — inherently sequential.  Here the
-// lex-sorted unique A is turned into an explicit binary radix (Patricia) tree
-// in parallel (Karras, HPG 2012: node i of N-1 internal nodes is found from
-// longest-common-prefix lengths of neighbouring keys by binary search, no
-// inter-thread communication), each node annotated with its subtree's
-// minimum cardinality.  Every query set y is then handled by one thread that
-// walks the tree depth-first:
+// lex-sorted unique A becomes an explicit binary radix (Patricia) tree built
+// in parallel (Karras, HPG 2012: internal node i is found from the longest
+// common prefixes of neighbouring keys by binary search, no inter-thread
+// communication), each node annotated with its subtree's min cardinality.
+// A query y walks the tree depth-first:
 //   * a node's keys agree on bits < lcp; bits [d, lcp) of that common prefix
 //     must lie in y (else the subtree is dead);
 //   * at the split bit L the 0-child is always admissible, the 1-child only if
 //     y has state L (exactly the reference's "ones side recurses with B_1");
 //   * subtrees whose min cardinality exceeds |y| (|y|-1 for proper) are cut —
 //     the reference's per-pair card filter lifted to whole subtrees;
-//   * ranges of <= kBrute keys are scanned linearly (contiguous rows).
-// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} is independent of
+//   * ranges of <= kPoolBrute keys are scanned (warp-cooperatively).
+// The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} does not depend on the
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
 
@@ -34,9 +33,8 @@ struct __align__(16) Node {
   uint16_t minc;    // min cardinality in the range
 };
 
+
 constexpr u32 kLeafBit = 0x80000000u;
-constexpr int kBrute = 12;
-constexpr int kStack = 64;
 
 template <int W>
 __device__ __forceinline__ int key_delta(const u64* __restrict__ A, long long N, long long i,
@@ -129,138 +127,152 @@ ContainIndex build_index(Context& c, const DList& a) {
   return ix;
 }
 
+// ---------------------------------------------------------------------------
+// Query-side layout.  Both sides of a query are private copies (the index's
+// relabelled sorted keys, the relabelled queries), so they use a padded row
+// of P = even(W+1) words with the cardinality stored in word W: a row and its
+// card arrive in P/2 16-byte vector loads.  (The L1/TEX pipe, not DRAM, is
+// what bounds the traversal — ncu: 92% L1/TEX throughput, 99% L2 hit.)
 template <int W>
-__device__ __forceinline__ bool is_subset(const u64* __restrict__ x, const u64 (&y)[W]) {
+struct Row {
+  static constexpr int P = (W + 2) & ~1;
+};
+
+template <int W>
+__device__ __forceinline__ void load_row(const u64* __restrict__ base, u64 idx, u64 (&x)[W],
+                                         u32& card) {
+  constexpr int P = Row<W>::P;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(base + idx * P);
+#pragma unroll
+  for (int i = 0; i < P / 2; ++i) {
+    const ulonglong2 v = __ldg(p + i);
+    if (2 * i < W) x[2 * i] = v.x;
+    if (2 * i == W) card = static_cast<u32>(v.x);
+    if (2 * i + 1 < W) x[2 * i + 1] = v.y;
+    if (2 * i + 1 == W) card = static_cast<u32>(v.y);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ bool is_subset(const u64 (&x)[W], const u64 (&y)[W]) {
   u64 acc = 0;
 #pragma unroll
   for (int w = 0; w < W; ++w) acc |= x[w] & ~y[w];
   return acc == 0;
 }
 
-// One thread per query y.  EXIST: stop everything at the first hit (meet
-// check / DFS trie query); otherwise write keep[j] = !hit.
-template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(128) contain_query_kernel(
-    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
-    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u64 Nb,
-    uint8_t* __restrict__ keep, int* found, unsigned long long* wit) {
-  const u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-  if (j >= Nb) return;
-  if (EXIST && *reinterpret_cast<volatile int*>(found)) return;
-  u64 y[W];
+// Relabel states (bit q -> bit pos[q]) and write rows in the padded layout
+// (PAD) or the plain W-word layout + card array.
+template <int W, bool PAD>
+__global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
+                               u32 n, const uint16_t* __restrict__ g_pos, u64* __restrict__ dst,
+                               u32* __restrict__ dcard) {
+  extern __shared__ uint16_t s_pos[];
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x) s_pos[q] = g_pos[q];
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 acc[W];
 #pragma unroll
-  for (int w = 0; w < W; ++w) y[w] = B[j * W + w];
-  const u32 cy = Bcard[j];
-  bool hit = false;
-  u32 hit_a = 0;
-  if (Na > 0 && !(PROPER && cy == 0)) {
-    const u32 limit = PROPER ? cy - 1 : cy;
-    u32 st_id[kStack];
-    uint16_t st_d[kStack];
-    int sp = 0;
-    st_id[sp] = Na == 1 ? kLeafBit : 0u;
-    st_d[sp++] = 0;
-    u32 iter = 0;
-    while (sp > 0 && !hit) {
-      if (EXIST && ((++iter & 63) == 0) && *reinterpret_cast<volatile int*>(found)) break;
-      --sp;
-      const u32 id = st_id[sp];
-      const int d = st_d[sp];
-      if (id & kLeafBit) {
-        const u32 x = id & ~kLeafBit;
-        if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-          hit = true;
-          hit_a = x;
-        }
-        continue;
-      }
-      const Node nd = nodes[id];
-      if (nd.minc > limit) continue;
-      if (nd.last - nd.first < kBrute) {
-        for (u32 x = nd.first; x <= nd.last; ++x)
-          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-            hit = true;
-            hit_a = x;
-            break;
-          }
-        continue;
-      }
-      const int L = nd.lcp;
-      // Bits [d, L) are common to the whole range: they must lie in y.
-      const u64* xf = A + static_cast<u64>(nd.first) * W;
-      u64 bad = 0;
+    for (int w = 0; w < W; ++w) acc[w] = 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-      if (bad) continue;
-      const u32 left = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-      const u32 right = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-      const bool y_has_L = (y[L >> 6] >> (63 - (L & 63))) & 1;
-      if (sp + 2 > kStack) {
-        // Stack exhausted (very deep tree): finish this subtree linearly.
-        for (u32 x = nd.first; x <= nd.last; ++x)
-          if (Acard[x] <= limit && is_subset<W>(A + static_cast<u64>(x) * W, y)) {
-            hit = true;
-            hit_a = x;
-            break;
-          }
-        continue;
+    for (int w = 0; w < W; ++w) {
+      u64 bits = src[i * W + w];
+      while (bits) {
+        const int b = __clzll(bits);
+        bits &= ~(u64{1} << (63 - b));
+        const u32 t = s_pos[w * 64 + b];
+        const u64 m = u64{1} << (63 - (t & 63));
+#pragma unroll
+        for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == (t >> 6)) ? m : 0;
       }
-      if (y_has_L) {
-        st_id[sp] = right;
-        st_d[sp++] = static_cast<uint16_t>(L + 1);
-      }
-      st_id[sp] = left;
-      st_d[sp++] = static_cast<uint16_t>(L + 1);
     }
-  }
-  if (EXIST) {
-    if (hit && atomicCAS(found, 0, 1) == 0) {
-      wit[0] = hit_a;
-      wit[1] = j;
+    if (PAD) {
+      constexpr int P = Row<W>::P;
+#pragma unroll
+      for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? acc[w] : (w == W ? scard[i] : 0);
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) dst[i * W + w] = acc[w];
+      dcard[i] = scard[i];
     }
-  } else {
-    keep[j] = hit ? 0 : 1;
   }
 }
 
+// Plain sorted rows -> padded rows.
+template <int W>
+__global__ void pad_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
+                           u64* __restrict__ dst) {
+  constexpr int P = Row<W>::P;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? src[i * W + w] : (w == W ? scard[i] : 0);
+  }
+}
+
+__global__ void state_hist_kernel(const u64* __restrict__ words, u64 count, u32 W, u32 n,
+                                  u32* __restrict__ hist) {
+  extern __shared__ u32 sh[];
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count * W;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 bits = words[i];
+    const u32 base = static_cast<u32>(i % W) * 64;
+    while (bits) {
+      const int b = __clzll(bits);
+      bits &= ~(u64{1} << (63 - b));
+      atomicAdd(&sh[base + b], 1u);
+    }
+  }
+  __syncthreads();
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x)
+    if (sh[q]) atomicAdd(&hist[q], sh[q]);
+}
+
 // ---------------------------------------------------------------------------
-// Warp-cooperative work-pool traversal (the production query kernel).
+// Warp-cooperative work-pool traversal.
 //
-// Per-query traversal lengths are heavy-tailed (n=300: mean ~1e3 node visits,
-// p99 ~8e3, max ~6e4), so one-thread-per-query leaves warps waiting on their
-// slowest lane and a small query batch (the meet check: ~2e4 queries) runs
-// for the serial latency of its longest walk.  Here every warp owns a LIFO
-// pool of (query, node, depth) tasks in shared memory.  Each round the 32
-// lanes pop 32 tasks — from any mix of queries — test them, and push the
-// admissible children back with ballot-compacted stores; when the pool holds
-// fewer than 32 tasks the warp pulls new queries from a global counter.
-// Long queries are thereby spread over all lanes, short ones pack densely,
-// and the grid is persistent (a fixed number of CTAs per SM).
+// Per-query walks are heavy-tailed (n=300: mean ~1e3 node visits, p99 ~8e3,
+// max ~6e4), so one-thread-per-query leaves warps waiting on their slowest
+// lane and a small batch (the meet check: ~2e4 queries) runs for the serial
+// latency of its longest walk.  Every warp owns a LIFO pool of tasks
+// (query j, node, first key of the node's range, next bit d | |y|) in shared
+// memory.  Each round the lanes pop up to 32 tasks from any mix of queries,
+// load node + node's first key + query row in ONE concurrent round of 16-B
+// vector loads, and push the admissible children with ballot-compacted
+// stores; when fewer than 32 tasks remain the warp pulls new queries from a
+// global counter (persistent grid).  Small ranges are scanned cooperatively:
+// all (range, key) pairs of the warp are flattened over the lanes
+// (consecutive keys → coalesced rows), the owner's y broadcast by shuffles.
+// MARK mode: hits also go to a per-warp table so sibling tasks of a marked
+// query are dropped without touching global memory.
 constexpr int kPoolWarps = 6;
 constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 512;  // tasks per warp
-constexpr int kPoolBrute = 16; // ranges of <= this many keys are scanned cooperatively
+constexpr int kPoolCap = 480;   // tasks per warp (static smem <= 48 KB per block)
+constexpr int kPoolBrute = 16;  // ranges of <= this many keys are scanned
+constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
 
-// A task is (query j, tree node id | kLeafBit, first key of the node's range,
-// next bit to check).  Carrying `first` lets the node record, the node's
-// first key (prefix check), the query row and the flags load concurrently:
-// one memory round trip per task.
 template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
-    const u64* __restrict__ A, const u32* __restrict__ Acard, const Node* __restrict__ nodes,
-    u32 Na, const u64* __restrict__ B, const u32* __restrict__ Bcard, u32 Nb,
-    uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
+    const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
+    u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
-  __shared__ uint16_t s_d[kPoolWarps][kPoolCap];
+  __shared__ u32 s_dc[kPoolWarps][kPoolCap];  // d | |y| << 16
+  __shared__ u32 s_hit[kPoolWarps][kHitSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
   u32* sq = s_q[wid];
   u32* sn = s_n[wid];
   u32* sf = s_f[wid];
-  uint16_t* sd = s_d[wid];
+  u32* sdc = s_dc[wid];
+  u32* shit = s_hit[wid];
+  shit[lane] = kNone;
+  __syncwarp();
   const u32 root_id = Na == 1 ? kLeafBit : 0u;
   int sp = 0;
   bool more = true;
@@ -274,14 +286,15 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       if (base + (32 - sp) >= Nb) more = false;
       const u32 j = base + lane;
       bool push = static_cast<u32>(lane) < got;
-      if (push && PROPER && Bcard[j] == 0) push = false;
+      const u32 cy = push ? static_cast<u32>(B[static_cast<u64>(j) * Row<W>::P + W]) : 0;
+      if (PROPER && cy == 0) push = false;
       const unsigned m = __ballot_sync(FULL, push);
       if (push) {
         const int pos = sp + __popc(m & lt);
         sq[pos] = j;
         sn[pos] = root_id;
         sf[pos] = 0;
-        sd[pos] = 0;
+        sdc[pos] = cy << 16;
       }
       sp += __popc(m);
       __syncwarp();
@@ -292,46 +305,41 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     }
     const int take = sp < 32 ? sp : 32;
     bool have = lane < take;
-    u32 j = 0, id = 0, first = 0;
-    int d = 0;
+    u32 j = 0, id = 0, first = 0, dc = 0;
     if (have) {
       const int pos = sp - 1 - lane;
       j = sq[pos];
       id = sn[pos];
       first = sf[pos];
-      d = sd[pos];
+      dc = sdc[pos];
     }
     sp -= take;
     __syncwarp();
+    if (!EXIST && have && shit[j % kHitSlots] == j) have = false;
+    const int d = static_cast<int>(dc & 0xFFFF);
+    const u32 cy = dc >> 16;
+    const u32 limit = PROPER ? cy - 1 : cy;
+    const bool is_leaf = (id & kLeafBit) != 0;
 
     // ---- one concurrent round of loads
     u64 y[W], xf[W];
-    u32 cy = 0, kcard = 0;
+    u32 ycard = 0, kcard = 0;
     Node nd{};
-    bool alive = have;
     if (have) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) y[w] = B[static_cast<u64>(j) * W + w];
-#pragma unroll
-      for (int w = 0; w < W; ++w) xf[w] = A[static_cast<u64>(first) * W + w];
-      cy = Bcard[j];
-      if (id & kLeafBit) kcard = Acard[first];
-      else nd = nodes[id];
-      if (!EXIST && *reinterpret_cast<volatile uint8_t*>(keep + j) == 0) alive = false;
+      load_row<W>(B, j, y, ycard);
+      load_row<W>(A, first, xf, kcard);
+      if (!is_leaf) nd = nodes[id];
     } else {
 #pragma unroll
       for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
     }
-    const u32 limit = PROPER ? cy - 1 : cy;
 
     // ---- evaluate the task
-    bool hit = false;
-    u32 hit_a = 0;
-    u32 c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
-    bool brute = false;
+    bool hit = false, brute = false;
+    u32 hit_a = 0, c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
     int dchild = 0;
-    if (alive) {
-      if (id & kLeafBit) {
+    if (have) {
+      if (is_leaf) {
         if (kcard <= limit && is_subset<W>(xf, y)) {
           hit = true;
           hit_a = first;
@@ -347,11 +355,10 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
 #pragma unroll
           for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
           if (!bad) {
-            const bool lleaf = nd.split == nd.first, rleaf = nd.split + 1 == nd.last;
-            c0 = lleaf ? (kLeafBit | nd.first) : nd.split;
+            c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
             f0 = nd.first;
             if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
-              c1 = rleaf ? (kLeafBit | nd.last) : nd.split + 1;
+              c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
               f1 = nd.split + 1;
             }
             dchild = L + 1;
@@ -363,6 +370,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     }
 
     // ---- push children (LIFO; left on top)
+    const u32 cdc = (cy << 16) | static_cast<u32>(dchild);
     const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
     const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
     const int n0 = __popc(m0), n1 = __popc(m1);
@@ -374,21 +382,20 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
         sq[pos] = j;
         sn[pos] = c1;
         sf[pos] = f1;
-        sd[pos] = static_cast<uint16_t>(dchild);
+        sdc[pos] = cdc;
       }
       if (c0 != kNone) {
         const int pos = sp + n1 + __popc(m0 & lt);
         sq[pos] = j;
         sn[pos] = c0;
         sf[pos] = f0;
-        sd[pos] = static_cast<uint16_t>(dchild);
+        sdc[pos] = cdc;
       }
       sp += n0 + n1;
     }
     __syncwarp();
 
-    // ---- cooperative scan of small ranges: all (range, key) pairs of the warp
-    // are flattened and spread over the lanes, 32 independent key tests per pass.
+    // ---- cooperative scan of small ranges: (range, key) pairs flattened over lanes
     const u32 cnt = brute ? bl - bf + 1 : 0;
     u32 incl = cnt;
 #pragma unroll
@@ -416,11 +423,9 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       for (int w = 0; w < W; ++w) oy[w] = __shfl_sync(FULL, y[w], owner);
       if (t < total) {
         const u32 key = o_bf + (t - o_excl);
-        // card and row issued together: one memory round trip per pass
-        const u32 kc = Acard[key];
         u64 kr[W];
-#pragma unroll
-        for (int w = 0; w < W; ++w) kr[w] = A[static_cast<u64>(key) * W + w];
+        u32 kc = 0;
+        load_row<W>(A, key, kr, kc);
         if (kc <= o_lim && is_subset<W>(kr, oy)) {
           if (EXIST) {
             if (atomicCAS(found, 0, 1) == 0) {
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
             }
           } else {
             keep[o_j] = 0;
+            shit[o_j % kHitSlots] = o_j;
           }
         }
       }
@@ -441,125 +447,51 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
         }
       } else {
         keep[j] = 0;
+        shit[j % kHitSlots] = j;
       }
     }
     __syncwarp();
   }
 }
 
+// keep[j] = !hit (MARK) or *found/wit (EXIST) for padded queries Bp against
+// the padded keys of index p.
 template <bool PROPER, bool EXIST>
-static void launch_query(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
-                         uint8_t* keep, int* found, unsigned long long* wit) {
-  const u64 Nb = b.size();
+static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, uint8_t* keep,
+                         int* found, unsigned long long* wit) {
   if (!Nb) return;
   cudaStream_t s = as_stream(c.stream());
   if (!EXIST) SW_CUDA(cudaMemsetAsync(keep, 1, Nb, s));
-  if (a.empty()) return;
-  u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..3)
+  if (p.count == 0) return;
+  u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..5)
   SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    int dev = 0;
-    SW_CUDA(cudaGetDevice(&dev));
-    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SW_DISPATCH_W(c.W(), {
-      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
-    });
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  int sms = 0, blocks_per_sm = 0, dev = 0;
+  SW_CUDA(cudaGetDevice(&dev));
+  SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SW_DISPATCH_W(c.W(), {
+    SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
+  });
+  blocks_per_sm = std::max(1, blocks_per_sm);
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
-        a.words, a.cards, static_cast<const Node*>(ia.nodes), static_cast<u32>(a.size()), b.words,
-        b.cards, static_cast<u32>(Nb), keep, found, wit, counter);
+        p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
+        static_cast<u32>(Nb), keep, found, wit, counter);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
 }
 
-size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper) {
-  if (b.empty() || a.empty()) return 0;
-  const size_t before = b.size();
-  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
-  if (proper)
-    launch_query<true, false>(c, a, ia, b, keep, nullptr, nullptr);
-  else
-    launch_query<false, false>(c, a, ia, b, keep, nullptr, nullptr);
-  return before - compact_flags(c, b, keep, nullptr);
-}
-
-std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
-                                   bool proper) {
-  std::vector<uint8_t> out(b.size(), 1);
-  if (b.empty() || a.empty()) return out;
-  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
-  if (proper)
-    launch_query<true, false>(c, a, ia, b, keep, nullptr, nullptr);
-  else
-    launch_query<false, false>(c, a, ia, b, keep, nullptr, nullptr);
-  c.memcpy_d2h(out.data(), keep, b.size());
-  return out;
-}
-
-// ------------------------------------------------------- state relabelling
-__global__ void state_hist_kernel(const u64* __restrict__ words, u64 count, u32 W, u32 n,
-                                  u32* __restrict__ hist) {
-  extern __shared__ u32 sh[];
-  for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
-  __syncthreads();
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count * W;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    u64 bits = words[i];
-    const u32 base = static_cast<u32>(i % W) * 64;
-    while (bits) {
-      const int b = __clzll(bits);
-      bits &= ~(u64{1} << (63 - b));
-      atomicAdd(&sh[base + b], 1u);
-    }
-  }
-  __syncthreads();
-  for (u32 q = threadIdx.x; q < n; q += blockDim.x)
-    if (sh[q]) atomicAdd(&hist[q], sh[q]);
-}
-
-template <int W>
-__global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
-                               u32 n, const uint16_t* __restrict__ g_pos, u64* __restrict__ dst,
-                               u32* __restrict__ dcard) {
-  extern __shared__ uint16_t s_pos[];
-  for (u32 q = threadIdx.x; q < n; q += blockDim.x) s_pos[q] = g_pos[q];
-  __syncthreads();
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    u64 acc[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) acc[w] = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      u64 bits = src[i * W + w];
-      while (bits) {
-        const int b = __clzll(bits);
-        bits &= ~(u64{1} << (63 - b));
-        const u32 t = s_pos[w * 64 + b];
-        const u64 m = u64{1} << (63 - (t & 63));
-#pragma unroll
-        for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == (t >> 6)) ? m : 0;
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < W; ++w) dst[i * W + w] = acc[w];
-    dcard[i] = scard[i];
-  }
-}
-
+// ------------------------------------------------------- relabelled index
 PermIndex::~PermIndex() {
   if (ctx) {
     try {
       ctx->free(orig);
       ctx->free(state_pos);
+      ctx->free(keys);
     } catch (...) {
     }
   }
@@ -570,25 +502,30 @@ PermIndex& PermIndex::operator=(PermIndex&& o) noexcept {
     if (ctx) {
       ctx->free(orig);
       ctx->free(state_pos);
+      ctx->free(keys);
     }
     ctx = o.ctx;
-    sorted = std::move(o.sorted);
+    count = o.count;
     orig = o.orig;
     state_pos = o.state_pos;
+    keys = o.keys;
     tree = std::move(o.tree);
     o.orig = nullptr;
     o.state_pos = nullptr;
+    o.keys = nullptr;
+    o.count = 0;
   }
   return *this;
 }
 
-DList relabel(Context& c, const DList& l, const PermIndex& p) {
-  DList out(&c, l.size(), false);
-  out.set_size(l.size());
-  if (l.empty()) return out;
+// Relabelled copy of l: padded rows (queries) or a plain list.
+static u64* relabel_padded(Context& c, const DList& l, const uint16_t* pos) {
+  u64* out = nullptr;
   SW_DISPATCH_W(c.W(), {
-    relabel_kernel<W><<<grid_for(l.size(), 256, 148 * 8), 256, c.n() * 2, as_stream(c.stream())>>>(
-        l.words, l.cards, l.size(), c.n(), p.state_pos, out.words, out.cards);
+    out = static_cast<u64*>(c.alloc(std::max<size_t>(l.size(), 1) * Row<W>::P * 8));
+    if (!l.empty())
+      relabel_kernel<W, true><<<grid_for(l.size(), 256, 148 * 8), 256, c.n() * 2, as_stream(c.stream())>>>(
+          l.words, l.cards, l.size(), c.n(), pos, out, nullptr);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches++;
@@ -598,6 +535,7 @@ DList relabel(Context& c, const DList& l, const PermIndex& p) {
 PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   PermIndex p;
   p.ctx = &c;
+  p.count = a.size();
   const u32 n = c.n();
   cudaStream_t s = as_stream(c.stream());
   std::vector<uint16_t> pos(n);
@@ -605,8 +543,8 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   if (order != StateOrder::Natural && !a.empty()) {
     u32* hist = static_cast<u32*>(c.alloc(n * 4));
     SW_CUDA(cudaMemsetAsync(hist, 0, n * 4, s));
-    state_hist_kernel<<<grid_for(a.size() * c.W(), 256, 148 * 2), 256, n * 4, s>>>(a.words, a.size(), c.W(), n,
-                                                                                   hist);
+    state_hist_kernel<<<grid_for(a.size() * c.W(), 256, 148 * 2), 256, n * 4, s>>>(a.words, a.size(),
+                                                                                   c.W(), n, hist);
     SW_CHECK_LAUNCH();
     std::vector<u32> h(n);
     c.memcpy_d2h(h.data(), hist, n * 4);
@@ -621,68 +559,91 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   }
   p.state_pos = static_cast<uint16_t*>(c.alloc(n * 2));
   c.memcpy_h2d(p.state_pos, pos.data(), n * 2);
-  p.sorted = std::make_unique<DList>(relabel(c, a, p));
+  // Relabel, sort (lex, in the new state order), pad.
+  DList sorted(&c, a.size(), false);
+  sorted.set_size(a.size());
+  if (!a.empty()) {
+    SW_DISPATCH_W(c.W(), {
+      relabel_kernel<W, false><<<grid_for(a.size(), 256, 148 * 8), 256, n * 2, s>>>(
+          a.words, a.cards, a.size(), n, p.state_pos, sorted.words, sorted.cards);
+    });
+    SW_CHECK_LAUNCH();
+  }
   p.orig = static_cast<u32*>(c.alloc(std::max<size_t>(a.size(), 1) * 4));
   if (a.size() > 1) {
-    const u32* perm = sort_perm(c, *p.sorted, false);
+    const u32* perm = sort_perm(c, sorted, false);
     SW_CUDA(cudaMemcpyAsync(p.orig, perm, a.size() * 4, cudaMemcpyDeviceToDevice, s));
-    compact_flags(c, *p.sorted, nullptr, p.orig);
+    compact_flags(c, sorted, nullptr, p.orig);
   } else if (a.size() == 1) {
     SW_CUDA(cudaMemsetAsync(p.orig, 0, 4, s));
   }
-  p.tree = build_index(c, *p.sorted);
+  p.tree = build_index(c, sorted);
+  SW_DISPATCH_W(c.W(), {
+    p.keys = static_cast<u64*>(c.alloc(std::max<size_t>(a.size(), 1) * Row<W>::P * 8));
+    if (!a.empty())
+      pad_kernel<W><<<grid_for(a.size(), 256, 148 * 8), 256, 0, s>>>(sorted.words, sorted.cards, a.size(),
+                                                                    p.keys);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 3;
   return p;
 }
 
 bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
-  if (!p.sorted || p.sorted->empty() || b.empty()) return false;
-  const DList rb = relabel(c, b, p);
-  Witness tw;
-  if (!exists_subset(c, *p.sorted, p.tree, rb, &tw)) return false;
-  if (w) {
-    u32 o = 0;
-    c.memcpy_d2h(&o, p.orig + tw.a_index, 4);
-    w->a_index = o;
-    w->b_index = tw.b_index;
-  }
-  return true;
-}
-
-size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper) {
-  if (b.empty() || !p.sorted || p.sorted->empty()) return 0;
-  const DList rb = relabel(c, b, p);
-  const size_t before = b.size();
-  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
-  if (proper)
-    launch_query<true, false>(c, *p.sorted, p.tree, rb, keep, nullptr, nullptr);
-  else
-    launch_query<false, false>(c, *p.sorted, p.tree, rb, keep, nullptr, nullptr);
-  return before - compact_flags(c, b, keep, nullptr);
-}
-
-size_t self_reduce_minimal(Context& c, DList& l) {
-  if (l.size() <= 1) return 0;
-  const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
-  return remove_supersets(c, p, l, /*proper=*/true);
-}
-
-bool exists_subset(Context& c, const DList& a, const ContainIndex& ia, const DList& b, Witness* w) {
-  if (a.empty() || b.empty()) return false;
+  if (p.count == 0 || b.empty()) return false;
+  u64* Bp = relabel_padded(c, b, p.state_pos);
   struct Res {
     int found;
     int pad;
     unsigned long long wit[2];
   };
-  auto* d = static_cast<Res*>(c.scratch(7, sizeof(Res)));
+  auto* d = static_cast<Res*>(c.scratch(7, 64));
   SW_CUDA(cudaMemsetAsync(d, 0, sizeof(Res), as_stream(c.stream())));
-  launch_query<false, true>(c, a, ia, b, nullptr, &d->found, d->wit);
+  launch_query<false, true>(c, p, Bp, b.size(), nullptr, &d->found, d->wit);
   Res h;
   c.memcpy_d2h(&h, d, sizeof(Res));
+  c.free(Bp);
   if (h.found && w) {
-    w->a_index = h.wit[0];
+    u32 o = 0;
+    c.memcpy_d2h(&o, p.orig + h.wit[0], 4);
+    w->a_index = o;
     w->b_index = h.wit[1];
   }
   return h.found != 0;
+}
+
+static uint8_t* keep_flags(Context& c, const PermIndex& p, const DList& b, bool proper) {
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+  u64* Bp = relabel_padded(c, b, p.state_pos);
+  if (proper)
+    launch_query<true, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
+  else
+    launch_query<false, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
+  c.free(Bp);
+  return keep;
+}
+
+size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper) {
+  if (b.empty() || p.count == 0) return 0;
+  const size_t before = b.size();
+  uint8_t* keep = keep_flags(c, p, b, proper);
+  return before - compact_flags(c, b, keep, nullptr);
+}
+
+std::vector<uint8_t> superset_keep(Context& c, const PermIndex& p, const DList& b, bool proper) {
+  std::vector<uint8_t> out(b.size(), 1);
+  if (b.empty() || p.count == 0) return out;
+  uint8_t* keep = keep_flags(c, p, b, proper);
+  c.memcpy_d2h(out.data(), keep, b.size());
+  return out;
+}
+
+// Minimal antichain: drop every set with a proper subset in the list.
+// Rarest-state-first order prunes best here (queries are the keys themselves).
+size_t self_reduce_minimal(Context& c, DList& l) {
+  if (l.size() <= 1) return 0;
+  const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
+  return remove_supersets(c, p, l, /*proper=*/true);
 }
 
 }  // namespace synchro::dev

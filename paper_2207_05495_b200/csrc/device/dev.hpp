@@ -162,15 +162,15 @@ size_t dedupe_sorted(Context& c, DList& l);            // returns #removed
 size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
 
 // ---- containment (subset_algebra.hpp:138-231, static_trie.hpp:51-55)
-ContainIndex build_index(Context& c, const DList& a);  // a lex-sorted unique
-// Removes every b element that is a superset (proper: strict superset) of
-// some a element; b keeps its order.  Returns #removed.
-size_t remove_supersets(Context& c, const DList& a, const ContainIndex& ia, DList& b, bool proper);
-// Containment index over A with the states relabelled so that the radix tree
-// splits first on the states that prune best for the expected queries:
+// Radix tree over a lex-sorted unique list (internal building block).
+ContainIndex build_index(Context& c, const DList& a);
+// Containment index over a duplicate-free A.  A is copied with its states
+// relabelled so that the radix tree splits first on the states that prune
+// best for the expected queries:
 //   FreqDesc — most frequent state of A first (queries sparser than A:
 //              meet check, DFS trie query; ~2.5x fewer visits at n=300),
-//   FreqAsc  — rarest first (self-reduction; ~1.3x fewer visits).
+//   FreqAsc  — rarest first (self-reduction; ~1.3x fewer visits),
+//   Natural  — identity.
 // The relabelling is a bijection, so containment (and every size) is
 // unchanged; witness indices are mapped back to A's original positions.
 enum class StateOrder { Natural, FreqDesc, FreqAsc };
@@ -180,24 +180,22 @@ struct PermIndex {
   PermIndex(PermIndex&&) noexcept;
   PermIndex& operator=(PermIndex&&) noexcept;
   Context* ctx = nullptr;
-  std::unique_ptr<DList> sorted;  // relabelled, lex-sorted unique copy of A
+  size_t count = 0;               // |A|
+  u64* keys = nullptr;            // relabelled sorted A, padded rows (card in word W)
   u32* orig = nullptr;            // sorted position -> index in A
   uint16_t* state_pos = nullptr;  // state q -> relabelled position
-  ContainIndex tree;
+  ContainIndex tree;              // radix tree over the relabelled sorted keys
 };
 PermIndex build_perm_index(Context& c, const DList& a, StateOrder order);
-DList relabel(Context& c, const DList& l, const PermIndex& p);  // same order, untagged
+// Is some A element a subset of some b element?  (meet_check / trie query)
 bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w);
+// Removes every b element that is a superset (proper: strict superset) of
+// some A element; b keeps its order.  Returns #removed.
 size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper);
-
-// keep[j] = 1 iff b[j] is not a (proper) superset of any a element.
-std::vector<uint8_t> superset_keep(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
-                                   bool proper);
+// keep[j] = 1 iff b[j] is not a (proper) superset of any A element.
+std::vector<uint8_t> superset_keep(Context& c, const PermIndex& p, const DList& b, bool proper);
 // Self-reduction to the minimal antichain (subset_algebra.hpp:179-197).
 size_t self_reduce_minimal(Context& c, DList& l);
-// Is some a element a subset of some b element?  (meet_check / trie query)
-bool exists_subset(Context& c, const DList& a, const ContainIndex& ia, const DList& b,
-                   Witness* w);
 
 // ---- list surgery
 void keep_card_at_most(Context& c, DList& l, u32 max_card);

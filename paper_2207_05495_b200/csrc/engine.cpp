@@ -192,8 +192,8 @@ void GpuBibfs::bfs_step(bool with_history) {
   double r_hist = 0.0;
   if (with_history) {
     const size_t before = next.size();
-    const dev::ContainIndex hix = dev::build_index(ctx_, *hbfs_);
-    const size_t removed = dev::remove_supersets(ctx_, *hbfs_, hix, next, /*proper=*/false);
+    const dev::PermIndex hix = dev::build_perm_index(ctx_, *hbfs_, dev::StateOrder::FreqDesc);
+    const size_t removed = dev::remove_supersets(ctx_, hix, next, /*proper=*/false);
     r_hist = ratio(removed, before);
   }
   shrink_charge(next.size());
@@ -238,8 +238,8 @@ void GpuBibfs::ibfs_step(bool with_history) {
   double r_hist = 0.0;
   if (with_history) {
     const size_t before = next.size();
-    const dev::ContainIndex hix = dev::build_index(ctx_, *hibfs_c_);
-    const size_t removed = dev::remove_supersets(ctx_, *hibfs_c_, hix, next, /*proper=*/false);
+    const dev::PermIndex hix = dev::build_perm_index(ctx_, *hibfs_c_, dev::StateOrder::FreqDesc);
+    const size_t removed = dev::remove_supersets(ctx_, hix, next, /*proper=*/false);
     r_hist = ratio(removed, before);
   }
   shrink_charge(next.size());
@@ -342,9 +342,9 @@ class DfsRunner {
       DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
       dev::complement(c_, largest);
       dev::lex_sort_dedupe(c_, largest);
-      const dev::ContainIndex lix = dev::build_index(c_, largest);
+      const dev::PermIndex lix = dev::build_perm_index(c_, largest, dev::StateOrder::FreqDesc);
       dev::complement(c_, next);
-      dev::remove_supersets(c_, largest, lix, next, /*proper=*/true);
+      dev::remove_supersets(c_, lix, next, /*proper=*/true);
       dev::complement(c_, next);
     }
     const u64 now = list_footprint(n, next.size());
