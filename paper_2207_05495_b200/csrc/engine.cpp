@@ -5,6 +5,7 @@
 #include <sstream>
 
 #include "device/dev.hpp"
+#include "progress.hpp"
 
 namespace synchro {
 namespace detail {
@@ -353,6 +354,9 @@ class DfsRunner {
       guard.amount = now;
     }
     if (log_) log_->push_back({r, level, hi - lo, generated, next.size()});
+    SYNCHRO_PROGRESS("dfs r=%llu level=%u in=%zu generated=%llu kept=%zu",
+                     static_cast<unsigned long long>(r), level, hi - lo,
+                     static_cast<unsigned long long>(generated), next.size());
     dev::Witness w;
     if (dev::exists_subset(c_, index_, next, tracking_ ? &w : nullptr)) {
       bound_ = r;
@@ -496,6 +500,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
     R = heur->length;
   }
   res.upper_bound = R;
+  SYNCHRO_PROGRESS("n=%u k=%u upper bound R=%llu", aut.state_count(), aut.alphabet_size(),
+                   static_cast<unsigned long long>(R));
   const auto t1 = clock::now();
   res.heuristic_seconds = std::chrono::duration<double>(t1 - t0).count();
 
@@ -577,6 +583,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
     else
       ++res.ibfs_steps;
     detail::trace_line(opt.trace, eng, st, sc, kind);
+    SYNCHRO_PROGRESS("iter %llu %s -> |L_BFS|=%zu |L_IBFS|=%zu", static_cast<unsigned long long>(r),
+                     step_kind_name(kind), eng.bfs_size(), eng.ibfs_size());
 
     if (opt.track_word) {
       size_t bi = 0;
