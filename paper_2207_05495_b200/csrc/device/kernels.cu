@@ -82,6 +82,121 @@ __global__ void __launch_bounds__(256) expand_kernel(
   }
 }
 
+// ------------------------------------------------------ bit-sliced expansion
+// A warp takes 64 parents at a time and transposes them into per-state bit
+// slices (slice[q] bit 63-i = "parent i contains q", a 64x64 bit transpose per
+// word done with 5 shuffle stages), so both actions become word-wide gathers
+// over 64 sets at once:
+//   preimage  out[p] = slice[delta(p,a)]                       (1 load / state)
+//   image     out[t] = OR_{q : delta(q,a) = t} slice[q]         (CSR of delta^-1)
+// and transposes the result back into child rows.  Lane l computes exactly
+// the output slices 64w+l and 64w+32+l it needs for the inverse transpose,
+// so outputs never leave registers.  ~10 warp-instructions per child instead
+// of a divergent per-lane loop over set bits.
+
+// 32x32 bit transposes of the two halves of x across the warp (row = lane,
+// MSB-first columns), by recursive block swaps.
+__device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
+  constexpr u64 kM[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
+                         0x3333333333333333ull, 0x5555555555555555ull};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const u64 m = kM[s];
+    const u64 y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & m) | ((y & m) << j)) : ((x & ~m) | ((y & ~m) >> j));
+  }
+  return x;
+}
+
+// 64x64 transpose: lane l holds rows l and l+32 (r0, r1); returns columns
+// l and l+32 (c0, c1), MSB-first in both orientations (an involution).
+__device__ __forceinline__ void transpose64(u64 r0, u64 r1, int lane, u64& c0, u64& c1) {
+  const u64 t0 = transpose32x2(r0, lane);  // [A^T_l | B^T_l]
+  const u64 t1 = transpose32x2(r1, lane);  // [C^T_l | D^T_l]
+  c0 = (t0 & 0xFFFFFFFF00000000ull) | (t1 >> 32);
+  c1 = (t0 << 32) | (t1 & 0xFFFFFFFFull);
+}
+
+constexpr int kSliceWarps = 4;
+
+template <int W, bool INV>
+__global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
+    const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
+    const uint16_t* __restrict__ g_img, const u32* __restrict__ g_off,
+    const uint16_t* __restrict__ g_src, u64* __restrict__ out, u32* __restrict__ out_card,
+    u64* __restrict__ out_tag) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const u32 kn = k * n;
+  u64* s_slices = reinterpret_cast<u64*>(smem);  // [warps][64W]
+  unsigned char* tab = smem + kSliceWarps * 64 * W * sizeof(u64);
+  u32* s_off = reinterpret_cast<u32*>(tab);
+  uint16_t* s_tab = INV ? reinterpret_cast<uint16_t*>(tab) : reinterpret_cast<uint16_t*>(s_off + kn + 1);
+  if (INV) {
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
+  } else {
+    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_src[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
+  const u64 batches = (count + 63) / 64;
+  for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
+       b += static_cast<u64>(gridDim.x) * kSliceWarps) {
+    const u64 i0 = b * 64 + lane, i1 = i0 + 32;
+    const bool v0 = i0 < count, v1 = i1 < count;
+    // ---- parents -> slices
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 r0 = v0 ? __ldg(src + (lo + i0) * W + w) : 0;
+      const u64 r1 = v1 ? __ldg(src + (lo + i1) * W + w) : 0;
+      u64 c0, c1;
+      transpose64(r0, r1, lane, c0, c1);
+      sl[64 * w + lane] = c0;
+      sl[64 * w + 32 + lane] = c1;
+    }
+    __syncwarp();
+    for (u32 a = 0; a < k; ++a) {
+      const u32 base = a * n;
+      u32 card0 = 0, card1 = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        u64 s[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const u32 p = 64 * w + 32 * h + lane;
+          u64 acc = 0;
+          if (p < n) {
+            if (INV) {
+              acc = sl[s_tab[base + p]];
+            } else {
+              const u32 e1 = s_off[base + p + 1];
+              for (u32 e = s_off[base + p]; e < e1; ++e) acc |= sl[s_tab[e]];
+            }
+          }
+          s[h] = acc;
+        }
+        u64 r0, r1;
+        transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
+        if (v0) out[(i0 * k + a) * W + w] = r0;
+        if (v1) out[(i1 * k + a) * W + w] = r1;
+        card0 += __popcll(r0);
+        card1 += __popcll(r1);
+      }
+      if (v0) {
+        out_card[i0 * k + a] = card0;
+        if (out_tag) out_tag[i0 * k + a] = ((lo + i0) << 16) | a;
+      }
+      if (v1) {
+        out_card[i1 * k + a] = card1;
+        if (out_tag) out_tag[i1 * k + a] = ((lo + i1) << 16) | a;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DList& out) {
   const size_t cnt = hi > lo ? hi - lo : 0;
   const u32 k = c.k(), n = c.n();
@@ -89,7 +204,7 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   out.set_size(cnt * k);
   if (!cnt) return;
   const size_t kn = static_cast<size_t>(k) * n;
-  const size_t shmem = inverse ? (kn + 1) * 4 + kn * 2 : kn * 2;
+  const size_t tab_bytes = inverse ? kn * 2 : (kn + 1) * 4 + kn * 2;
   cudaStream_t s = as_stream(c.stream());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.timing) {
@@ -97,10 +212,12 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
     SW_CUDA(cudaEventCreate(&e1));
     SW_CUDA(cudaEventRecord(e0, s));
   }
-  const int block = 256;
-  const int grid = grid_for(cnt, block, 148 * 8);
+  const int block = kSliceWarps * 32;
+  const u64 batches = (cnt + 63) / 64;
+  const int grid = static_cast<int>(std::min<u64>((batches + kSliceWarps - 1) / kSliceWarps, 148 * 16));
   SW_DISPATCH_W(c.W(), {
-    auto kern = inverse ? expand_kernel<W, true> : expand_kernel<W, false>;
+    const size_t shmem = kSliceWarps * 64 * W * sizeof(u64) + ((tab_bytes + 15) & ~size_t{15});
+    auto kern = inverse ? expand_sliced_kernel<W, true> : expand_sliced_kernel<W, false>;
     if (shmem > 48 * 1024)
       SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(shmem)));
