@@ -23,6 +23,7 @@
 #include "dev.hpp"
 #include "kernels.cuh"
 #include "util.cuh"
+#include "../progress.hpp"
 
 namespace synchro::dev {
 
@@ -476,6 +477,11 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
+  std::unique_ptr<StreamTimer> timer;
+  if (progress_enabled()) {
+    timer = std::make_unique<StreamTimer>(c);
+    timer->start();
+  }
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
@@ -483,6 +489,10 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
+  if (timer)
+    SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms", EXIST ? "exist" : "mark",
+                     PROPER ? "-proper" : "", p.count, static_cast<unsigned long long>(Nb),
+                     timer->stop_ms());
 }
 
 // ------------------------------------------------------- relabelled index

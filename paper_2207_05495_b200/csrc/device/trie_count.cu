@@ -19,6 +19,7 @@
 #include "dev.hpp"
 #include "kernels.cuh"
 #include "util.cuh"
+#include "../progress.hpp"
 
 namespace synchro::dev {
 
@@ -230,6 +231,8 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
   c.free(per);
   c.free(ctr);
   if (hist) c.free(hist);
+  SYNCHRO_PROGRESS("  trie node count over %llu sets: %llu nodes", static_cast<unsigned long long>(N64),
+                   static_cast<unsigned long long>(h.nodes));
   return h.nodes;
 }
 
