@@ -388,10 +388,12 @@ SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
     dev::Context c(identity_aut(n));
     dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
-    if (mode == 2) {  // subsets of a ⟺ supersets among complements
-      dev::complement(c, a);
-      dev::lex_sort_dedupe(c, a);
-      dev::complement(c, b);
+    if (mode == 2) {  // subsets of some a element: the bucketed superset join
+      uint8_t* dkeep = static_cast<uint8_t*>(c.alloc(std::max<size_t>(b_count, 1)));
+      dev::superset_keep_flags(c, a, b, /*proper=*/false, dkeep);
+      c.memcpy_d2h(keep, dkeep, b_count);
+      c.free(dkeep);
+      return;
     }
     const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
     const std::vector<uint8_t> k = dev::superset_keep(c, ix, b, mode == 1);

@@ -212,26 +212,6 @@ __global__ void pad_kernel(const u64* __restrict__ src, const u32* __restrict__ 
   }
 }
 
-__global__ void state_hist_kernel(const u64* __restrict__ words, u64 count, u32 W, u32 n,
-                                  u32* __restrict__ hist) {
-  extern __shared__ u32 sh[];
-  for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
-  __syncthreads();
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count * W;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    u64 bits = words[i];
-    const u32 base = static_cast<u32>(i % W) * 64;
-    while (bits) {
-      const int b = __clzll(bits);
-      bits &= ~(u64{1} << (63 - b));
-      atomicAdd(&sh[base + b], 1u);
-    }
-  }
-  __syncthreads();
-  for (u32 q = threadIdx.x; q < n; q += blockDim.x)
-    if (sh[q]) atomicAdd(&hist[q], sh[q]);
-}
-
 // ---------------------------------------------------------------------------
 // Warp-cooperative work-pool traversal.
 //
@@ -552,10 +532,7 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   for (u32 q = 0; q < n; ++q) pos[q] = static_cast<uint16_t>(q);
   if (order != StateOrder::Natural && !a.empty()) {
     u32* hist = static_cast<u32*>(c.alloc(n * 4));
-    SW_CUDA(cudaMemsetAsync(hist, 0, n * 4, s));
-    state_hist_kernel<<<grid_for(a.size() * c.W(), 256, 148 * 2), 256, n * 4, s>>>(a.words, a.size(),
-                                                                                   c.W(), n, hist);
-    SW_CHECK_LAUNCH();
+    state_histogram(c, a, hist);
     std::vector<u32> h(n);
     c.memcpy_d2h(h.data(), hist, n * 4);
     c.free(hist);

@@ -194,6 +194,14 @@ bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w);
 size_t remove_supersets(Context& c, const PermIndex& p, DList& b, bool proper);
 // keep[j] = 1 iff b[j] is not a (proper) superset of any A element.
 std::vector<uint8_t> superset_keep(Context& c, const PermIndex& p, const DList& b, bool proper);
+// Superset join on plain sets (the dense / complement-space marking of the
+// reference rephrased): removes every y of Y that is a subset (proper: strict
+// subset) of some x of X; Y keeps its order.  Returns #removed.  (join.cu)
+size_t remove_subsets_of(Context& c, const DList& X, DList& Y, bool proper);
+// keep[j] = 1 iff Y[j] is not a (proper) subset of any X element (device array).
+void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper, uint8_t* keep);
+// Keeps the maximal sets of l (== self_reduce_minimal on the complements).
+size_t self_reduce_maximal(Context& c, DList& l);
 // Self-reduction to the minimal antichain (subset_algebra.hpp:179-197).
 size_t self_reduce_minimal(Context& c, DList& l);
 

@@ -92,31 +92,7 @@ __global__ void __launch_bounds__(256) expand_kernel(
 // and transposes the result back into child rows.  Lane l computes exactly
 // the output slices 64w+l and 64w+32+l it needs for the inverse transpose,
 // so outputs never leave registers.  ~10 warp-instructions per child instead
-// of a divergent per-lane loop over set bits.
-
-// 32x32 bit transposes of the two halves of x across the warp (row = lane,
-// MSB-first columns), by recursive block swaps.
-__device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
-  constexpr u64 kM[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
-                         0x3333333333333333ull, 0x5555555555555555ull};
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int j = 16 >> s;
-    const u64 m = kM[s];
-    const u64 y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
-    x = (lane & j) ? ((x & m) | ((y & m) << j)) : ((x & ~m) | ((y & ~m) >> j));
-  }
-  return x;
-}
-
-// 64x64 transpose: lane l holds rows l and l+32 (r0, r1); returns columns
-// l and l+32 (c0, c1), MSB-first in both orientations (an involution).
-__device__ __forceinline__ void transpose64(u64 r0, u64 r1, int lane, u64& c0, u64& c1) {
-  const u64 t0 = transpose32x2(r0, lane);  // [A^T_l | B^T_l]
-  const u64 t1 = transpose32x2(r1, lane);  // [C^T_l | D^T_l]
-  c0 = (t0 & 0xFFFFFFFF00000000ull) | (t1 >> 32);
-  c1 = (t0 << 32) | (t1 & 0xFFFFFFFFull);
-}
+// of a divergent per-lane loop over set bits.  (transpose64: util.cuh)
 
 constexpr int kSliceWarps = 4;
 
@@ -240,6 +216,50 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+}
+
+// ----------------------------------------------------------- state histogram
+// Each warp bit-slices 64 sets per word (transpose64) and popcounts the
+// slices: lane l accumulates the counts of states 64w+l and 64w+32+l in
+// registers, one global atomic per state per warp at the end.
+template <int W>
+__global__ void __launch_bounds__(256) state_hist_kernel(const u64* __restrict__ words, u64 count,
+                                                         u32 n, u32* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5;
+  const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+  u32 cnt[W][2];
+#pragma unroll
+  for (int w = 0; w < W; ++w) cnt[w][0] = cnt[w][1] = 0;
+  for (u64 b = warp; b * 64 < count; b += nwarps) {
+    const u64 i0 = b * 64 + lane, i1 = i0 + 32;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 r0 = i0 < count ? __ldg(words + i0 * W + w) : 0;
+      const u64 r1 = i1 < count ? __ldg(words + i1 * W + w) : 0;
+      u64 c0, c1;
+      transpose64(r0, r1, lane, c0, c1);
+      cnt[w][0] += __popcll(c0);
+      cnt[w][1] += __popcll(c1);
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const u32 q0 = 64 * w + lane, q1 = q0 + 32;
+    if (q0 < n && cnt[w][0]) atomicAdd(&hist[q0], cnt[w][0]);
+    if (q1 < n && cnt[w][1]) atomicAdd(&hist[q1], cnt[w][1]);
+  }
+}
+
+void state_histogram(Context& c, const DList& l, u32* hist) {
+  cudaStream_t s = as_stream(c.stream());
+  SW_CUDA(cudaMemsetAsync(hist, 0, c.n() * 4, s));
+  if (l.empty()) return;
+  const u64 batches = (l.size() + 63) / 64;
+  const int grid = static_cast<int>(std::min<u64>((batches + 7) / 8, 148 * 8));
+  SW_DISPATCH_W(c.W(), { state_hist_kernel<W><<<grid, 256, 0, s>>>(l.words, l.size(), c.n(), hist); });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
 }
 
 // --------------------------------------------------------------- complement

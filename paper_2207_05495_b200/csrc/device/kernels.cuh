@@ -17,6 +17,10 @@ size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm)
 // Keep the first row of every run of equal rows in perm order (sorted input).
 size_t compact_unique(Context& c, DList& l, const u32* perm);
 
+// hist[q] = number of sets of l containing state q (q < n); hist is a device
+// array of n u32, overwritten.  Bit-sliced: 64 sets per warp transpose.
+void state_histogram(Context& c, const DList& l, u32* hist);
+
 // Stable permutation sorting l lexicographically (optionally by descending
 // cardinality first); returned pointer lives in scratch slot 2 or 3.
 const u32* sort_perm(Context& c, const DList& l, bool card_desc);

@@ -59,6 +59,32 @@ __device__ __forceinline__ u64 range_mask(int w, int s, int e) {
   return top << (64 - hi);
 }
 
+// 32x32 bit transposes of the two 32-bit halves of x across the warp (row =
+// lane, MSB-first columns), by five stages of recursive block swaps.
+__device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
+  constexpr u64 kM[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
+                         0x3333333333333333ull, 0x5555555555555555ull};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const u64 m = kM[s];
+    const u64 y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & m) | ((y & m) << j)) : ((x & ~m) | ((y & ~m) >> j));
+  }
+  return x;
+}
+
+// 64x64 bit transpose across a warp: lane l holds rows l and l+32 (r0, r1)
+// and receives columns l and l+32 (c0, c1); MSB-first in both orientations,
+// so the transform is an involution.  Used to bit-slice 64 sets at a time
+// (slice[q] bit 63-i = "set i contains state q").
+__device__ __forceinline__ void transpose64(u64 r0, u64 r1, int lane, u64& c0, u64& c1) {
+  const u64 t0 = transpose32x2(r0, lane);  // [A^T_l | B^T_l]
+  const u64 t1 = transpose32x2(r1, lane);  // [C^T_l | D^T_l]
+  c0 = (t0 & 0xFFFFFFFF00000000ull) | (t1 >> 32);
+  c1 = (t0 << 32) | (t1 & 0xFFFFFFFFull);
+}
+
 inline int grid_for(size_t items, int block, int max_blocks = 148 * 16) {
   size_t g = (items + block - 1) / block;
   if (g < 1) g = 1;

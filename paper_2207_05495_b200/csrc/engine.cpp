@@ -222,7 +222,10 @@ void GpuBibfs::ibfs_step(bool with_history) {
     const u64 before = list_footprint(n_, hibfs_i_.size);
     // keep complements whose plain cardinality n - c is >= min card of L_IBFS
     dev::keep_card_at_most(ctx_, *hibfs_c_, n_ - libfs_i_.min_card);
-    dev::self_reduce_minimal(ctx_, *hibfs_c_);
+    // minimal complements == maximal plain sets (superset join, plain space)
+    dev::complement(ctx_, *hibfs_c_);
+    dev::self_reduce_maximal(ctx_, *hibfs_c_);
+    dev::complement(ctx_, *hibfs_c_);
     refresh(*hibfs_c_, hibfs_i_);
     h_ibfs_last_reduced_ = hibfs_i_.size;
     ledger_.release(before - list_footprint(n_, hibfs_i_.size));
@@ -235,14 +238,20 @@ void GpuBibfs::ibfs_step(bool with_history) {
   const size_t generated = next.size();
   const double r_dupl = generated ? ratio(dev::lex_sort_dedupe(ctx_, next), generated) : 0.0;
   const size_t after_dupl = next.size();
-  const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
+  // The reductions of the reference run on complements (minimal sets there);
+  // on plain sets they are superset queries — done by the bucketed superset
+  // join, which keeps the complement-lex order of `next`.
+  dev::complement(ctx_, next);
+  const double r_self = ratio(dev::self_reduce_maximal(ctx_, next), after_dupl);
   double r_hist = 0.0;
   if (with_history) {
     const size_t before = next.size();
-    const dev::PermIndex hix = dev::build_perm_index(ctx_, *hibfs_c_, dev::StateOrder::FreqDesc);
-    const size_t removed = dev::remove_supersets(ctx_, hix, next, /*proper=*/false);
+    DList h_plain = dev::copy_list(ctx_, *hibfs_c_, false);
+    dev::complement(ctx_, h_plain);
+    const size_t removed = dev::remove_subsets_of(ctx_, h_plain, next, /*proper=*/false);
     r_hist = ratio(removed, before);
   }
+  dev::complement(ctx_, next);
   shrink_charge(next.size());
   if (with_history) merge_history(*hibfs_c_, hibfs_i_, next);
   dev::complement(ctx_, next);
@@ -340,13 +349,10 @@ class DfsRunner {
     if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
       // Drop sets that are proper subsets of one of the dfs_largest first
       // (largest) sets — proper-superset marking on complements.
-      DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
-      dev::complement(c_, largest);
-      dev::lex_sort_dedupe(c_, largest);
-      const dev::PermIndex lix = dev::build_perm_index(c_, largest, dev::StateOrder::FreqDesc);
-      dev::complement(c_, next);
-      dev::remove_supersets(c_, lix, next, /*proper=*/true);
-      dev::complement(c_, next);
+      // (the reference marks proper supersets among complements; on plain sets:
+      // drop y ⊊ z for a window set z — superset join, order kept)
+      const DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
+      dev::remove_subsets_of(c_, largest, next, /*proper=*/true);
     }
     const u64 now = list_footprint(n, next.size());
     if (now < charged) {
