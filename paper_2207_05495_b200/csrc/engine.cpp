@@ -2,6 +2,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <set>
 #include <sstream>
 
 #include "device/dev.hpp"
@@ -291,6 +294,18 @@ bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
 // -------------------------------------------------------------- DFS phase
 namespace {
 
+// Analysis aid: with SYNCHRO_DUMP_DIR set, lists are written as raw u64 words.
+void dump_list(dev::Context& c, const DList& l, const std::string& name) {
+  const char* dir = std::getenv("SYNCHRO_DUMP_DIR");
+  if (!dir || !*dir) return;
+  std::vector<u64> w(l.size() * c.W());
+  dev::download(c, l, w.data(), nullptr, nullptr);
+  if (FILE* f = std::fopen((std::string(dir) + "/" + name + ".u64").c_str(), "wb")) {
+    std::fwrite(w.data(), 8, w.size(), f);
+    std::fclose(f);
+  }
+}
+
 // Level-by-level inverse DFS below the frozen L_BFS (dfs_phase.hpp:47-177):
 // the recursion, slicing and ledger stay on the host; every level's
 // preimages, (card desc, lex) order, dedupe, window pruning and containment
@@ -360,6 +375,7 @@ class DfsRunner {
       guard.amount = now;
     }
     if (log_) log_->push_back({r, level, hi - lo, generated, next.size()});
+    if (dumped_.insert(r).second) dump_list(c_, next, "dfs_r" + std::to_string(r));
     SYNCHRO_PROGRESS("dfs r=%llu level=%u in=%zu generated=%llu kept=%zu",
                      static_cast<unsigned long long>(r), level, hi - lo,
                      static_cast<unsigned long long>(generated), next.size());
@@ -404,6 +420,7 @@ class DfsRunner {
   std::vector<std::array<u64, 5>>* log_;
   u64 bound_ = 0;
   DfsFind find_;
+  std::set<u64> dumped_;
 };
 
 }  // namespace
@@ -420,6 +437,8 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   const u64 trie_bytes = list_footprint(n_, lbfs_i_.size) + nodes * 24;
   ledger_.charge_or_throw(trie_bytes);
   ledger_.release(list_footprint(n_, lbfs_i_.size));
+  dump_list(ctx_, *lbfs_, "lbfs");
+  dump_list(ctx_, *libfs_, "libfs");
   const dev::PermIndex& index = bfs_index();
   DfsRunner dfs(ctx_, *lbfs_, index, ledger_, opt_.tuning, deadline_, opt_.track_word, log);
   const u64 final_bound = dfs.run(*libfs_, r, R_);
