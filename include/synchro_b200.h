@@ -69,6 +69,8 @@ typedef struct sw_solve_options {
   uint32_t reduce_cadence;  /* 3 */
   int32_t device;           /* CUDA device, -1: current */
   int32_t timing;           /* 1: time expansion kernels with CUDA events */
+  uint32_t dfs_shard_index; /* multi-GPU DFS partition: this process's share ... */
+  uint32_t dfs_shard_count; /* ... of L_IBFS (threshold = MIN over shards); 1 = whole */
 } sw_solve_options;
 
 /* SolveResult (bibfs_engine.hpp:50-59) + expansion counters and timings. */

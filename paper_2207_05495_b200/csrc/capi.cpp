@@ -91,6 +91,9 @@ SolveOptions to_options(const sw_solve_options* o) {
   s.tuning.dfs_reduce_cadence = o->reduce_cadence;
   s.device = o->device;
   s.timing = o->timing != 0;
+  s.dfs_shard_count = std::max<uint32_t>(1, o->dfs_shard_count);
+  s.dfs_shard_index = o->dfs_shard_index;
+  if (s.dfs_shard_index >= s.dfs_shard_count) throw std::invalid_argument("dfs_shard_index >= dfs_shard_count");
   return s;
 }
 
@@ -126,6 +129,8 @@ SW_EXPORT void sw_default_options(sw_solve_options* o) {
   o->dedupe_cadence = 2;
   o->reduce_cadence = 3;
   o->device = -1;
+  o->dfs_shard_index = 0;
+  o->dfs_shard_count = 1;
 }
 
 SW_EXPORT int sw_random_automaton(uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta_out) {

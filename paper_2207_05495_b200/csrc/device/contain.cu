@@ -522,57 +522,11 @@ static u64* relabel_padded(Context& c, const DList& l, const uint16_t* pos) {
   return out;
 }
 
-template <int W>
-__global__ void pad_gather_kernel(const u64* __restrict__ src, const u32* __restrict__ scard,
-                                  const u32* __restrict__ perm, u64 count, u64* __restrict__ dst) {
-  constexpr int P = Row<W>::P;
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 s = perm[i];
-#pragma unroll
-    for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? src[s * W + w] : (w == W ? scard[s] : 0);
-  }
-}
-
 __global__ void scatter_flags_kernel(const uint8_t* __restrict__ src, const u32* __restrict__ perm,
                                      u64 count, uint8_t* __restrict__ dst) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<u64>(gridDim.x) * blockDim.x)
     dst[perm[i]] = src[i];
-}
-
-// Queries relabelled AND sorted lexicographically in the relabelled order, so
-// that the lanes of a warp walk neighbouring paths of the tree (locality once
-// the index outgrows L2, e.g. 1.7 GB of keys at n=570).  *perm_out[i] = the
-// original position of sorted query i (caller frees).
-static u64* relabel_sorted_padded(Context& c, const DList& l, const uint16_t* pos, u32** perm_out) {
-  cudaStream_t s = as_stream(c.stream());
-  DList tmp(&c, l.size(), false);
-  tmp.set_size(l.size());
-  u32* perm = static_cast<u32*>(c.alloc(std::max<size_t>(l.size(), 1) * 4));
-  u64* out = nullptr;
-  SW_DISPATCH_W(c.W(), {
-    out = static_cast<u64*>(c.alloc(std::max<size_t>(l.size(), 1) * Row<W>::P * 8));
-    if (!l.empty())
-      relabel_kernel<W, false><<<grid_for(l.size(), 256, 148 * 8), 256, c.n() * 2, s>>>(
-          l.words, l.cards, l.size(), c.n(), pos, tmp.words, tmp.cards);
-  });
-  SW_CHECK_LAUNCH();
-  if (l.size() > 1) {
-    const u32* sp = sort_perm(c, tmp, false);
-    SW_CUDA(cudaMemcpyAsync(perm, sp, l.size() * 4, cudaMemcpyDeviceToDevice, s));
-  } else if (l.size() == 1) {
-    SW_CUDA(cudaMemsetAsync(perm, 0, 4, s));
-  }
-  SW_DISPATCH_W(c.W(), {
-    if (!l.empty())
-      pad_gather_kernel<W><<<grid_for(l.size(), 256, 148 * 8), 256, 0, s>>>(tmp.words, tmp.cards, perm,
-                                                                           l.size(), out);
-  });
-  SW_CHECK_LAUNCH();
-  c.counters.kernel_launches += 2;
-  *perm_out = perm;
-  return out;
 }
 
 PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
@@ -631,8 +585,10 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
 
 bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
   if (p.count == 0 || b.empty()) return false;
-  u32* qperm = nullptr;
-  u64* Bp = relabel_sorted_padded(c, b, p.state_pos, &qperm);
+  // (Sorting the queries in relabelled-lex order was measured slower at n=570:
+  // heavy walks cluster into the same warps; the (card desc, lex) level order
+  // spreads them.)
+  u64* Bp = relabel_padded(c, b, p.state_pos);
   struct Res {
     int found;
     int pad;
@@ -645,30 +601,22 @@ bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
   c.memcpy_d2h(&h, d, sizeof(Res));
   c.free(Bp);
   if (h.found && w) {
-    u32 o = 0, q = 0;
+    u32 o = 0;
     c.memcpy_d2h(&o, p.orig + h.wit[0], 4);
-    c.memcpy_d2h(&q, qperm + h.wit[1], 4);
     w->a_index = o;
-    w->b_index = q;
+    w->b_index = h.wit[1];
   }
-  c.free(qperm);
   return h.found != 0;
 }
 
 static uint8_t* keep_flags(Context& c, const PermIndex& p, const DList& b, bool proper) {
   auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
-  uint8_t* ks = static_cast<uint8_t*>(c.alloc(b.size()));
-  u32* qperm = nullptr;
-  u64* Bp = relabel_sorted_padded(c, b, p.state_pos, &qperm);
+  u64* Bp = relabel_padded(c, b, p.state_pos);
   if (proper)
-    launch_query<true, false>(c, p, Bp, b.size(), ks, nullptr, nullptr);
+    launch_query<true, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
   else
-    launch_query<false, false>(c, p, Bp, b.size(), ks, nullptr, nullptr);
-  scatter_flags_kernel<<<grid_for(b.size(), 256), 256, 0, as_stream(c.stream())>>>(ks, qperm, b.size(), keep);
-  SW_CHECK_LAUNCH();
+    launch_query<false, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
   c.free(Bp);
-  c.free(qperm);
-  c.free(ks);
   return keep;
 }
 

@@ -318,12 +318,17 @@ class DfsRunner {
       : c_(c), lbfs_(lbfs), index_(index), ledger_(ledger), t_(t), deadline_(deadline),
         tracking_(tracking), log_(log) {}
 
-  u64 run(const DList& initial, u64 r0, u64 bound) {
+  // Shard s of c explores the subtrees of initial[begin, end) only, with
+  // [begin, end) the s-th of c contiguous, equal shares (c = 1: everything).
+  u64 run(const DList& initial, u64 r0, u64 bound, u32 shard = 0, u32 shards = 1) {
     bound_ = bound;
     if (r0 >= bound_ || initial.empty()) return bound_;
+    const size_t per = (initial.size() + shards - 1) / shards;
+    const size_t begin = std::min(initial.size(), static_cast<size_t>(shard) * per);
+    const size_t end = std::min(initial.size(), begin + per);
     const size_t cap = slice_cap(r0 - 1);
-    for (size_t lo = 0; lo < initial.size(); lo += cap) {
-      recurse(initial, lo, std::min(initial.size(), lo + cap), r0, 0, nullptr);
+    for (size_t lo = begin; lo < end; lo += cap) {
+      recurse(initial, lo, std::min(end, lo + cap), r0, 0, nullptr);
       if (r0 >= bound_) break;
     }
     return bound_;
@@ -441,7 +446,8 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   dump_list(ctx_, *libfs_, "libfs");
   const dev::PermIndex& index = bfs_index();
   DfsRunner dfs(ctx_, *lbfs_, index, ledger_, opt_.tuning, deadline_, opt_.track_word, log);
-  const u64 final_bound = dfs.run(*libfs_, r, R_);
+  const u64 final_bound =
+      dfs.run(*libfs_, r, R_, opt_.dfs_shard_index, std::max<u32>(1, opt_.dfs_shard_count));
   if (find) *find = dfs.find();
   if (expansions) *expansions = dfs.expansions;
   ledger_.release(trie_bytes);

@@ -52,6 +52,11 @@ struct SolveOptions {
   std::optional<u64> upper_bound{};
   int device = -1;      // CUDA device (-1: current)
   bool timing = false;  // CUDA-event timing of the expansion kernels
+  // Multi-GPU DFS partitioning (one process per GPU): this solve explores
+  // only the DFS subtrees rooted in its contiguous share of L_IBFS; the
+  // threshold of the whole search is the MIN over the shards.
+  u32 dfs_shard_index = 0;
+  u32 dfs_shard_count = 1;
 };
 
 struct SolveResult {

@@ -69,6 +69,7 @@ class SolveOptions(C.Structure):
         ("dfs_set_weight", C.c_double), ("dfs_check_weight", C.c_double),
         ("min_brute", C.c_uint32), ("min_leaf", C.c_uint32), ("dedupe_cadence", C.c_uint32),
         ("reduce_cadence", C.c_uint32), ("device", C.c_int32), ("timing", C.c_int32),
+        ("dfs_shard_index", C.c_uint32), ("dfs_shard_count", C.c_uint32),
     ]
 
 
