@@ -229,9 +229,26 @@ def run_ours(args, world, rank, local):
     last = e2e[-1][1]
     assert last.word is not None and len(last.word) == last.threshold and sw.is_reset_word(aut, last.word)
 
-    roof_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
-        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    roof_peak = json.load(open(peaks_path))["hbm_gbs"] if os.path.exists(peaks_path) else 6650.0
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if os.path.exists(peaks_path)
+                else "fallback 6650 GB/s (B200_PROFILING.md)")
     achieved = exp_children * exp_bytes_per_child / (exp_ms / 1e3) / 1e9 if exp_ms > 0 else None
+    engine_ms = sum(r.engine_device_ms for r in results)
+    cont_ms = sum(r.contain_kernel_ms for r in results)
+    cont_bytes = sum(r.contain_bytes for r in results)
+    cont_gbs = cont_bytes / (cont_ms / 1e3) / 1e9 if cont_ms > 0 else None
+    # HBM-scale microbenchmarks of the north-star kernels (2^24
+    # random subsets at the measured frontier density, under the workload automaton).
+    mb_count, mb_density = 1 << 24, 0.077
+    mb_exp_ms = sw.bench_expand(aut, mb_count, mb_density, seed=1, inverse=False, iters=5)
+    mb_pre_ms = sw.bench_expand(aut, mb_count, mb_density, seed=1, inverse=True, iters=5)
+    mb_exp_gbs = mb_count * aut.k * exp_bytes_per_child / (mb_exp_ms / 1e3) / 1e9
+    mb_pre_gbs = mb_count * aut.k * exp_bytes_per_child / (mb_pre_ms / 1e3) / 1e9
+    dd_ms, dd_unique = sw.bench_dedupe(aut.n, mb_count, mb_density, seed=1, dup_fraction=0.1, iters=3)
+    row = 8 * W + 4
+    dd_bytes = mb_count * row + dd_unique * row  # read every candidate once + write survivors once
+    dd_gbs = dd_bytes / (dd_ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": dev_s_max * 1e3 / args.steps,
@@ -251,11 +268,30 @@ def run_ours(args, world, rank, local):
                 "time_to_threshold_s": statistics.median(x[0] for x in e2e),
                 "note": "sw_solve_exact from a host delta table, adaptive heuristic included, "
                         "word read back and verified"},
-        "roofline": {"bound": "hbm", "kernel": "expand_kernel (image/preimage)",
-                     "achieved": achieved, "peak": roof_peak, "unit": "GB/s",
-                     "frac": (achieved / roof_peak) if achieved else None, "traffic": None,
-                     "bytes_per_unit": exp_bytes_per_child,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        # Dominant kernel of the step: the containment traversal (self-reduction,
+        # meet check, DFS queries).  Algorithmic bytes = every key and query row
+        # read once; it is a latency-bound tree walk (ncu: L1/TEX-throughput bound,
+        # profiles/), so its HBM fraction is small by nature.
+        "roofline": {"bound": "hbm", "kernel": "contain_pool_kernel (containment traversal)",
+                     "achieved": cont_gbs, "peak": roof_peak, "unit": "GB/s",
+                     "frac": (cont_gbs / roof_peak) if cont_gbs else None,
+                     "traffic": None, "share_of_step": cont_ms / engine_ms if engine_ms else None,
+                     "bytes_per_unit": f"{row} B per key/query row", "peak_source": peak_src},
+        # North-star kernels at HBM scale (2^24 parents, n=300, density 0.077).
+        "roofline_expand": {"bound": "hbm", "kernel": "expand_sliced_kernel",
+                            "achieved": mb_exp_gbs, "achieved_preimage": mb_pre_gbs,
+                            "peak": roof_peak, "unit": "GB/s", "frac": mb_exp_gbs / roof_peak,
+                            "frac_preimage": mb_pre_gbs / roof_peak,
+                            "bytes_per_unit": exp_bytes_per_child,
+                            "ms_per_launch": mb_exp_ms, "children_per_launch": mb_count * aut.k,
+                            "in_engine_achieved": achieved,
+                            "in_engine_share_of_step": exp_ms / engine_ms if engine_ms else None},
+        "roofline_dedupe": {"bound": "hbm", "kernel": "lex sort (CUB onesweep LSD) + unique "
+                                                       "warp-ballot compaction",
+                            "achieved": dd_gbs, "peak": roof_peak, "unit": "GB/s",
+                            "frac": dd_gbs / roof_peak, "ms_per_call": dd_ms,
+                            "sets": mb_count, "unique": dd_unique,
+                            "bytes_per_unit": f"{row} B read per candidate + {row} B per survivor"},
         "gpu_launches": launches,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

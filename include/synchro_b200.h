@@ -94,6 +94,8 @@ typedef struct sw_solve_result {
   double engine_device_ms;  /* CUDA-event span of the engine on its stream */
   uint64_t h2d_bytes;       /* host->device bytes copied during the solve */
   uint64_t d2h_bytes;       /* device->host bytes copied during the solve */
+  double contain_kernel_ms; /* CUDA-event time of the containment traversal (timing=1) */
+  uint64_t contain_bytes;   /* its algorithmic bytes (every key/query row read once) */
 } sw_solve_result;
 
 const char* sw_version(void);
@@ -185,6 +187,15 @@ int sw_step_costs(const double* stats, const int32_t* flags, const double* tunin
 
 int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t min_leaf,
                        uint64_t* nodes);
+
+/* ---- kernel microbenchmarks at HBM scale (bench.py roofline): `count` random
+ * sets of ~density*n states generated on the device; avg CUDA-event ms per
+ * call of the expansion kernel / of lex sort + dedupe (dup_fraction of the
+ * sets are duplicates). ---- */
+int sw_bench_expand(uint32_t n, uint32_t k, const uint32_t* delta, uint64_t count, double density,
+                    uint64_t seed, int32_t inverse, int32_t iters, double* ms);
+int sw_bench_dedupe(uint32_t n, uint64_t count, double density, uint64_t seed, double dup_fraction,
+                    int32_t iters, double* ms, uint64_t* unique_out);
 
 /* ---- experiment runner (experiment.hpp:133-188) → CSV file ---- */
 int sw_run_experiment(const uint32_t* ns, size_t ns_count, uint32_t k, uint32_t samples,

@@ -204,6 +204,8 @@ SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
     out->engine_seconds = r.engine_seconds;
     out->expand_kernel_ms = r.expand_kernel_ms;
     out->kernel_launches = r.kernel_launches;
+    out->contain_kernel_ms = r.contain_kernel_ms;
+    out->contain_bytes = r.contain_bytes;
     out->engine_device_ms = r.engine_device_ms;
     out->h2d_bytes = r.h2d_bytes;
     out->d2h_bytes = r.d2h_bytes;
@@ -418,6 +420,24 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
     const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
     *met = dev::exists_subset(c, ix, b, nullptr) ? 1 : 0;
+  });
+}
+
+SW_EXPORT int sw_bench_expand(uint32_t n, uint32_t k, const uint32_t* delta, uint64_t count,
+                              double density, uint64_t seed, int32_t inverse, int32_t iters,
+                              double* ms) {
+  return guarded([&] {
+    const Automaton aut = make_aut(n, k, delta);
+    dev::Context c(aut);
+    *ms = dev::bench_expand(c, count, density, seed, inverse != 0, std::max(1, iters));
+  });
+}
+
+SW_EXPORT int sw_bench_dedupe(uint32_t n, uint64_t count, double density, uint64_t seed,
+                              double dup_fraction, int32_t iters, double* ms, uint64_t* unique_out) {
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    *ms = dev::bench_dedupe(c, count, density, seed, dup_fraction, std::max(1, iters), unique_out);
   });
 }
 

@@ -458,7 +458,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
   std::unique_ptr<StreamTimer> timer;
-  if (progress_enabled()) {
+  if (progress_enabled() || c.timing) {
     timer = std::make_unique<StreamTimer>(c);
     timer->start();
   }
@@ -469,10 +469,16 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
-  if (timer)
+  if (timer) {
+    const double ms = timer->stop_ms();
+    // algorithmic bytes: every key and every query row read once, a flag written
+    const u64 row = static_cast<u64>(c.W()) * 8 + 4;
+    c.counters.contain_ms += ms;
+    c.counters.contain_launches += 1;
+    c.counters.contain_bytes += (p.count + Nb) * row + (EXIST ? 0 : Nb);
     SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms", EXIST ? "exist" : "mark",
-                     PROPER ? "-proper" : "", p.count, static_cast<unsigned long long>(Nb),
-                     timer->stop_ms());
+                     PROPER ? "-proper" : "", p.count, static_cast<unsigned long long>(Nb), ms);
+  }
 }
 
 // ------------------------------------------------------- relabelled index

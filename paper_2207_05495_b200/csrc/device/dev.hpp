@@ -87,6 +87,9 @@ struct Counters {
   u64 contain_pair_tests = 0;
   u64 h2d_bytes = 0;
   u64 d2h_bytes = 0;
+  double contain_ms = 0;   // CUDA-event time of the traversal kernel (when timed)
+  u64 contain_launches = 0;
+  u64 contain_bytes = 0;   // algorithmic bytes of those launches
 };
 
 // CUDA-event pair on a context's stream (device-side span of a region).
@@ -217,6 +220,12 @@ std::vector<u64> read_tags(Context& c, const DList& l);
 
 // ---- static trie shape (static_trie.hpp:85-151) for exact ledger accounting
 u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);
+
+// ---- microbenchmarks (microbench.cu): avg CUDA-event ms per call on `count`
+// device-generated random sets of the given density.
+double bench_expand(Context& c, u64 count, double density, u64 seed, bool inverse, int iters);
+double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_fraction, int iters,
+                    u64* unique_out);
 
 // Device count / properties.
 int device_count();

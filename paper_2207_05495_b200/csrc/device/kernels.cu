@@ -104,19 +104,14 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     u64* __restrict__ out_tag) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 kn = k * n;
-  u64* s_slices = reinterpret_cast<u64*>(smem);  // [warps][64W]
-  unsigned char* tab = smem + kSliceWarps * 64 * W * sizeof(u64);
-  u32* s_off = reinterpret_cast<u32*>(tab);
-  uint16_t* s_tab = INV ? reinterpret_cast<uint16_t*>(tab) : reinterpret_cast<uint16_t*>(s_off + kn + 1);
-  if (INV) {
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
-  } else {
-    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_src[i];
-  }
+  // [warps][64W] input slices, [warps][64W] output slices (image), table u16[k][n]
+  u64* s_slices = reinterpret_cast<u64*>(smem);
+  uint16_t* s_tab = reinterpret_cast<uint16_t*>(smem + 2 * kSliceWarps * 64 * W * sizeof(u64));
+  for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
+  u64* so = s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
   const u64 batches = (count + 63) / 64;
   for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
@@ -136,22 +131,25 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     for (u32 a = 0; a < k; ++a) {
       const u32 base = a * n;
       u32 card0 = 0, card1 = 0;
+      if (!INV) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
+#pragma unroll
+        for (int i = 0; i < 2 * W; ++i) so[32 * i + lane] = 0;
+        __syncwarp();
+        for (u32 q = lane; q < n; q += 32)
+          atomicOr(reinterpret_cast<unsigned long long*>(&so[s_tab[base + q]]),
+                   static_cast<unsigned long long>(sl[q]));
+        __syncwarp();
+      }
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         u64 s[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const u32 p = 64 * w + 32 * h + lane;
-          u64 acc = 0;
-          if (p < n) {
-            if (INV) {
-              acc = sl[s_tab[base + p]];
-            } else {
-              const u32 e1 = s_off[base + p + 1];
-              for (u32 e = s_off[base + p]; e < e1; ++e) acc |= sl[s_tab[e]];
-            }
-          }
-          s[h] = acc;
+          if (INV)
+            s[h] = p < n ? sl[s_tab[base + p]] : 0;  // preimage: pure gather
+          else
+            s[h] = so[p];
         }
         u64 r0, r1;
         transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
@@ -180,7 +178,7 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   out.set_size(cnt * k);
   if (!cnt) return;
   const size_t kn = static_cast<size_t>(k) * n;
-  const size_t tab_bytes = inverse ? kn * 2 : (kn + 1) * 4 + kn * 2;
+  const size_t tab_bytes = kn * 2;
   cudaStream_t s = as_stream(c.stream());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.timing) {
@@ -192,7 +190,7 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   const u64 batches = (cnt + 63) / 64;
   const int grid = static_cast<int>(std::min<u64>((batches + kSliceWarps - 1) / kSliceWarps, 148 * 16));
   SW_DISPATCH_W(c.W(), {
-    const size_t shmem = kSliceWarps * 64 * W * sizeof(u64) + ((tab_bytes + 15) & ~size_t{15});
+    const size_t shmem = 2 * kSliceWarps * 64 * W * sizeof(u64) + ((tab_bytes + 15) & ~size_t{15});
     auto kern = inverse ? expand_sliced_kernel<W, true> : expand_sliced_kernel<W, false>;
     if (shmem > 48 * 1024)
       SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

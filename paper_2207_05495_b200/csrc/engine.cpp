@@ -550,6 +550,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
     res.engine_seconds = std::chrono::duration<double>(clock::now() - t1).count();
     res.expand_kernel_ms = ctx.counters.expand_ms;
     res.kernel_launches = ctx.counters.kernel_launches;
+    res.contain_kernel_ms = ctx.counters.contain_ms;
+    res.contain_bytes = ctx.counters.contain_bytes;
     return res;
   };
 

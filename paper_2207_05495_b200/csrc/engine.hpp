@@ -75,6 +75,8 @@ struct SolveResult {
   double engine_seconds = 0;
   double expand_kernel_ms = 0;  // CUDA-event time of expansion kernels (when timed)
   u64 kernel_launches = 0;
+  double contain_kernel_ms = 0;  // CUDA-event time of the containment traversal (when timed)
+  u64 contain_bytes = 0;         // its algorithmic bytes (keys + queries read once)
   double engine_device_ms = 0;  // CUDA-event span of the engine on its stream
   u64 h2d_bytes = 0, d2h_bytes = 0;
   std::string phase;            // meet | dfs | bound | trivial

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = [
     "sw_list_expand", "sw_list_lex_sort_dedupe", "sw_list_sort_card_desc_lex",
     "sw_list_dedupe_sorted", "sw_list_self_reduce_minimal", "sw_list_mark",
     "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
-    "sw_step_costs",
+    "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe",
 ]
 
 
@@ -82,7 +82,7 @@ class SolveResultC(C.Structure):
         ("heuristic_seconds", C.c_double), ("engine_seconds", C.c_double),
         ("expand_kernel_ms", C.c_double), ("kernel_launches", C.c_uint64),
         ("phase", C.c_char * 16), ("engine_device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
-        ("d2h_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64), ("contain_kernel_ms", C.c_double), ("contain_bytes", C.c_uint64),
     ]
 
 
@@ -162,8 +162,29 @@ def load():
     _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
     _ip = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
     L.sw_step_costs.argtypes = [_dp, _ip, _dp, _dp, _dp, _ip, C.POINTER(C.c_int32)]
+    L.sw_bench_expand.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_uint64, C.c_double, C.c_uint64,
+                                  C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+    L.sw_bench_dedupe.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_int32,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
     _lib = L
     return L
+
+
+def bench_expand(aut, count: int, density: float, seed: int = 1, inverse: bool = False,
+                 iters: int = 5) -> float:
+    """Average ms of one expansion launch over `count` random parents (k children each)."""
+    ms = C.c_double()
+    _check(load().sw_bench_expand(aut.n, aut.k, aut.delta, count, density, seed, int(inverse), iters,
+                                  C.byref(ms)))
+    return ms.value
+
+
+def bench_dedupe(n: int, count: int, density: float, seed: int = 1, dup_fraction: float = 0.1,
+                 iters: int = 3):
+    """(avg ms of lex sort + dedupe over `count` random sets, unique count)."""
+    ms, u = C.c_double(), C.c_uint64()
+    _check(load().sw_bench_dedupe(n, count, density, seed, dup_fraction, iters, C.byref(ms), C.byref(u)))
+    return ms.value, u.value
 
 
 def exp_mark(a_size: float, b_size: float, a_density: float, b_density: float) -> float:
@@ -283,6 +304,8 @@ class SolveResult:
     engine_device_ms: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    contain_kernel_ms: float = 0.0
+    contain_bytes: int = 0
     trace: Optional[List[str]] = field(default=None)
 
     @property
@@ -322,7 +345,7 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
                        bool(r.used_dfs), r.peak_memory, r.expansions_phase1, r.expansions_dfs,
                        r.heuristic_seconds, r.engine_seconds, r.expand_kernel_ms,
                        r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
-                       r.d2h_bytes, trace)
+                       r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace)
 
 
 ALGORITHMS = {"eppstein": 0, "beam": 1, "adaptive": 2}
