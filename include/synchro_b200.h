@@ -195,7 +195,7 @@ int sw_trie_node_count(uint32_t n, const uint64_t* words, size_t count, uint32_t
 int sw_bench_expand(uint32_t n, uint32_t k, const uint32_t* delta, uint64_t count, double density,
                     uint64_t seed, int32_t inverse, int32_t iters, double* ms);
 int sw_bench_dedupe(uint32_t n, uint64_t count, double density, uint64_t seed, double dup_fraction,
-                    int32_t iters, double* ms, uint64_t* unique_out);
+                    int32_t iters, int32_t lex_sort, double* ms, uint64_t* unique_out);
 
 /* ---- experiment runner (experiment.hpp:133-188) → CSV file ---- */
 int sw_run_experiment(const uint32_t* ns, size_t ns_count, uint32_t k, uint32_t samples,

@@ -434,10 +434,12 @@ SW_EXPORT int sw_bench_expand(uint32_t n, uint32_t k, const uint32_t* delta, uin
 }
 
 SW_EXPORT int sw_bench_dedupe(uint32_t n, uint64_t count, double density, uint64_t seed,
-                              double dup_fraction, int32_t iters, double* ms, uint64_t* unique_out) {
+                              double dup_fraction, int32_t iters, int32_t lex_sort, double* ms,
+                              uint64_t* unique_out) {
   return guarded([&] {
     dev::Context c(identity_aut(n));
-    *ms = dev::bench_dedupe(c, count, density, seed, dup_fraction, std::max(1, iters), unique_out);
+    *ms = dev::bench_dedupe(c, count, density, seed, dup_fraction, std::max(1, iters), unique_out,
+                            lex_sort != 0);
   });
 }
 

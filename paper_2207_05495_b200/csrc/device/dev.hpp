@@ -163,6 +163,9 @@ void sort_lex(Context& c, DList& l);                   // stable, index tie-brea
 void sort_card_desc_lex(Context& c, DList& l);         // card desc, lex, index
 size_t dedupe_sorted(Context& c, DList& l);            // returns #removed
 size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
+// Set-semantics dedupe by open-addressing hash: keeps the first occurrence of
+// every distinct row, survivors in their original order.  Returns #removed.
+size_t hash_dedupe(Context& c, DList& l);
 
 // ---- containment (subset_algebra.hpp:138-231, static_trie.hpp:51-55)
 // Radix tree over a lex-sorted unique list (internal building block).
@@ -225,7 +228,7 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);
 // device-generated random sets of the given density.
 double bench_expand(Context& c, u64 count, double density, u64 seed, bool inverse, int iters);
 double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_fraction, int iters,
-                    u64* unique_out);
+                    u64* unique_out, bool lex_sort);
 
 // Device count / properties.
 int device_count();

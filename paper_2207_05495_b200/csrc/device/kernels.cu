@@ -470,6 +470,90 @@ size_t compact_unique(Context& c, DList& l, const u32* perm) {
   return r;
 }
 
+// ------------------------------------------------------------- hash dedupe
+// Open addressing over 2^m >= 2N slots of u64 = (32-bit row hash << 32 | row
+// index), linear probing.  Insert: claim an empty slot by CAS; on a slot with
+// the same hash tag compare rows, and for an equal row keep the MINIMUM index
+// (atomicMin on the packed value: equal rows share the tag) — the first
+// occurrence, i.e. the same duplicate the reference's stable lex sort keeps
+// (set_list.hpp:208-209).  Each row remembers its slot, so "am I the
+// survivor" is one table read, fused into the warp-ballot compaction.
+__device__ __forceinline__ u64 mix64(u64 x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+template <int W>
+__global__ void hash_insert_kernel(const u64* __restrict__ words, u64 count,
+                                   unsigned long long* table, u64 mask, u32* __restrict__ slot_of) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 row[W];
+    u64 h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      row[w] = words[i * W + w];
+      h = mix64(h ^ row[w]);
+    }
+    const u64 tag = h >> 32;
+    const unsigned long long mine = (tag << 32) | i;
+    u64 s = h & mask;
+    while (true) {
+      unsigned long long cur = table[s];
+      if (cur == ~0ull) {
+        cur = atomicCAS(&table[s], ~0ull, mine);
+        if (cur == ~0ull) break;  // claimed
+      }
+      if ((cur >> 32) == tag) {
+        const u64 j = cur & 0xFFFFFFFFull;
+        bool eq = true;
+#pragma unroll
+        for (int w = 0; w < W; ++w) eq &= words[j * W + w] == row[w];
+        if (eq) {
+          atomicMin(&table[s], mine);
+          break;
+        }
+      }
+      s = (s + 1) & mask;
+    }
+    slot_of[i] = static_cast<u32>(s);
+  }
+}
+
+struct KeepHashFirst {
+  const unsigned long long* table;
+  const u32* slot_of;
+  __device__ bool operator()(u64 i) const {
+    return (table[slot_of[i]] & 0xFFFFFFFFull) == i;
+  }
+};
+
+size_t hash_dedupe(Context& c, DList& l) {
+  const u64 N = l.size();
+  if (N <= 1) return 0;
+  if (N >= 0xFFFFFFFFull) throw std::invalid_argument("hash_dedupe: list too large");
+  u64 slots = 1;
+  while (slots < 2 * N) slots <<= 1;
+  cudaStream_t s = as_stream(c.stream());
+  auto* table = static_cast<unsigned long long*>(c.alloc(slots * 8));
+  auto* slot_of = static_cast<u32*>(c.alloc(N * 4));
+  SW_CUDA(cudaMemsetAsync(table, 0xFF, slots * 8, s));
+  size_t kept = 0;
+  SW_DISPATCH_W(c.W(), {
+    hash_insert_kernel<W><<<grid_for(N, 256, 148 * 16), 256, 0, s>>>(l.words, N, table, slots - 1, slot_of);
+    SW_CHECK_LAUNCH();
+    kept = run_compact<W>(c, l, KeepHashFirst{table, slot_of}, nullptr);
+  });
+  c.counters.kernel_launches += 2;
+  c.free(table);
+  c.free(slot_of);
+  return N - kept;
+}
+
 // ------------------------------------------------------ cardinality filters
 __global__ void card_filter_kernel(const u32* cards, u64 count, u32 bound, int at_least,
                                    uint8_t* keep) {

@@ -62,7 +62,7 @@ double bench_expand(Context& c, u64 count, double density, u64 seed, bool invers
 }
 
 double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_fraction, int iters,
-                    u64* unique_out) {
+                    u64* unique_out, bool lex_sort) {
   const DList src = random_sets(c, count, density, seed, dup_fraction);
   double total = 0;
   for (int i = 0; i <= iters; ++i) {
@@ -70,7 +70,10 @@ double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_
     c.sync();
     StreamTimer t(c);
     t.start();
-    lex_sort_dedupe(c, l);
+    if (lex_sort)
+      lex_sort_dedupe(c, l);
+    else
+      hash_dedupe(c, l);
     const double ms = t.stop_ms();
     if (i > 0) total += ms;  // i == 0: warm-up
     if (unique_out) *unique_out = l.size();

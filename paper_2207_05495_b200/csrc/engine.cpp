@@ -190,7 +190,10 @@ void GpuBibfs::bfs_step(bool with_history) {
   dev::expand(ctx_, *lbfs_, 0, lbfs_i_.size, /*inverse=*/false, next);
   Rollback rb{ledger_, charged_layer_};
   const size_t generated = next.size();
-  const double r_dupl = generated ? ratio(dev::lex_sort_dedupe(ctx_, next), generated) : 0.0;
+  // Set-semantics dedupe (hash; same survivors as the reference's stable lex
+  // sort + unique).  L_BFS needs no lex order: every consumer either sorts its
+  // own relabelled copy (containment index) or is order-free (stats, ledger).
+  const double r_dupl = generated ? ratio(dev::hash_dedupe(ctx_, next), generated) : 0.0;
   const size_t after_dupl = next.size();
   const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
   double r_hist = 0.0;

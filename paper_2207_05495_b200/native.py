@@ -165,7 +165,7 @@ def load():
     L.sw_bench_expand.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_uint64, C.c_double, C.c_uint64,
                                   C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     L.sw_bench_dedupe.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_int32,
-                                  C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+                                  C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
     _lib = L
     return L
 
@@ -180,10 +180,11 @@ def bench_expand(aut, count: int, density: float, seed: int = 1, inverse: bool =
 
 
 def bench_dedupe(n: int, count: int, density: float, seed: int = 1, dup_fraction: float = 0.1,
-                 iters: int = 3):
-    """(avg ms of lex sort + dedupe over `count` random sets, unique count)."""
+                 iters: int = 3, lex_sort: bool = False):
+    """(avg ms of the hash dedupe [or lex sort + dedupe] over `count` random sets, unique count)."""
     ms, u = C.c_double(), C.c_uint64()
-    _check(load().sw_bench_dedupe(n, count, density, seed, dup_fraction, iters, C.byref(ms), C.byref(u)))
+    _check(load().sw_bench_dedupe(n, count, density, seed, dup_fraction, iters, int(lex_sort),
+                                  C.byref(ms), C.byref(u)))
     return ms.value, u.value
 
 
