@@ -27,12 +27,24 @@
 
 namespace synchro::dev {
 
-struct __align__(16) Node {
+struct __align__(32) Node {
   u32 first, last;  // key range [first, last]
   u32 split;        // left = [first, split], right = [split+1, last]
   uint16_t lcp;     // first bit where the range's keys differ
   uint16_t minc;    // min cardinality in the range
+  u64 window;       // bits [lcp-64, lcp) of the range's keys (common prefix tail)
+  u64 pad;
 };
+
+// Bits [e-64, e) of an MSB-first bit string, right-aligned (bit e-1 at the
+// LSB; positions < 0 read as 0).  `at(w)` returns word w.
+template <class At>
+__device__ __forceinline__ u64 window_before(At at, int e) {
+  const int q = e >> 6, r = e & 63;
+  const u64 hi = q > 0 ? at(q - 1) : 0;
+  if (r == 0) return hi;
+  return (hi << r) | (at(q) >> (64 - r));
+}
 
 
 constexpr u32 kLeafBit = 0x80000000u;
@@ -77,6 +89,9 @@ __global__ void karras_kernel(const u64* __restrict__ A, u32 N, Node* __restrict
   nd.split = static_cast<u32>(gamma);
   nd.lcp = static_cast<uint16_t>(dnode);
   nd.minc = 0xFFFF;
+  const u64* key = A + static_cast<long long>(first) * W;
+  nd.window = window_before([&](int w) { return key[w]; }, dnode);
+  nd.pad = 0;
   nodes[i] = nd;
   if (first == gamma) parent_leaf[gamma] = static_cast<u32>(i);
   else parent_int[gamma] = static_cast<u32>(i);
@@ -306,13 +321,14 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     u64 y[W], xf[W];
     u32 ycard = 0, kcard = 0;
     Node nd{};
-    if (have) {
-      load_row<W>(B, j, y, ycard);
-      load_row<W>(A, first, xf, kcard);
-      if (!is_leaf) nd = nodes[id];
-    } else {
 #pragma unroll
-      for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
+    for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
+    if (have) {
+      // a node visit needs the node (its window covers the prefix check) and y;
+      // only a leaf (single key) needs the key row itself
+      load_row<W>(B, j, y, ycard);
+      if (is_leaf) load_row<W>(A, first, xf, kcard);
+      else nd = nodes[id];
     }
 
     // ---- evaluate the task
@@ -332,9 +348,25 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
           bl = nd.last;
         } else {
           const int L = nd.lcp;
+          const int need = L - d;  // common-prefix bits not yet checked
           u64 bad = 0;
+          if (need > 0 && need <= 64) {
+            const u64 yw = window_before(
+                [&](int q) {
+                  u64 v = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+                  for (int w = 0; w < W; ++w) v = (w == q) ? y[w] : v;
+                  return v;
+                },
+                L);
+            const u64 m = need == 64 ? ~u64{0} : ((u64{1} << need) - 1);
+            bad = nd.window & ~yw & m;
+          } else if (need > 64) {  // long common run: check against the key row
+            u32 kc;
+            load_row<W>(A, nd.first, xf, kc);
+#pragma unroll
+            for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+          }
           if (!bad) {
             c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
             f0 = nd.first;
