@@ -154,7 +154,8 @@ std::set<std::string> join(std::set<std::string> a, const std::set<std::string>&
 int cmd_exact(int argc, char** argv) {
   const Args a = parse_args(argc, argv, 2,
                             join(join(kSource, kTuning), {"--memory", "--time-limit", "--threads",
-                                                          "--schedule", "--trace", "--device"}),
+                                                          "--schedule", "--trace", "--device",
+                                                          "--dfs-shard"}),
                             {"--track-word"});
   SolveOptions opt;
   if (a.has("--memory")) opt.memory = to_u64(a.get("--memory"), "--memory");
@@ -167,6 +168,15 @@ int cmd_exact(int argc, char** argv) {
   else if (sched == "dfs") opt.schedule = Schedule::DfsImmediate;
   else if (sched != "auto") throw UsageError("--schedule: " + sched + " not in {auto,bfs,ibfs,dfs}");
   if (a.has("--device")) opt.device = static_cast<int>(to_u64(a.get("--device"), "--device"));
+  if (a.has("--dfs-shard")) {  // I/N: explore only the I-th of N shares of the DFS (multi-GPU)
+    const std::string v = a.get("--dfs-shard");
+    const auto slash = v.find('/');
+    if (slash == std::string::npos) throw UsageError("--dfs-shard expects I/N");
+    opt.dfs_shard_index = static_cast<u32>(to_u64(v.substr(0, slash), "--dfs-shard"));
+    opt.dfs_shard_count = static_cast<u32>(to_u64(v.substr(slash + 1), "--dfs-shard"));
+    if (opt.dfs_shard_count == 0 || opt.dfs_shard_index >= opt.dfs_shard_count)
+      throw UsageError("--dfs-shard expects I/N with I < N");
+  }
   if (a.has("--threads")) to_u64(a.get("--threads"), "--threads");  // accepted, as in the reference
   const Automaton aut = load_automaton(a);
   apply_tuning(a, opt.tuning);
