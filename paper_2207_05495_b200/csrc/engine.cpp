@@ -367,13 +367,19 @@ class DfsRunner {
     dev::expand(c_, list, lo, hi, /*inverse=*/true, next);
     expansions += static_cast<u64>(hi - lo) * k;
     const u64 generated = next.size();
-    dev::sort_card_desc_lex(c_, next);
-    if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0) dev::dedupe_sorted(c_, next);
+    // The reference sorts every level by (card desc, lex, index) (dfs_phase.hpp:105).
+    // The order is observable only through the top-dfs_largest window and the
+    // slice boundaries, so it is materialised only when one of those happens;
+    // the dedupe is set-semantic (first occurrence survives, as after the
+    // stable sort), and the trie query is order-free.
+    bool sorted = false;
+    if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0) dev::hash_dedupe(c_, next);
     if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
       // Drop sets that are proper subsets of one of the dfs_largest first
-      // (largest) sets — proper-superset marking on complements.
-      // (the reference marks proper supersets among complements; on plain sets:
-      // drop y ⊊ z for a window set z — superset join, order kept)
+      // (largest) sets.  The reference marks proper supersets among
+      // complements; on plain sets it is a superset join (order kept).
+      dev::sort_card_desc_lex(c_, next);
+      sorted = true;
       const DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
       dev::remove_subsets_of(c_, largest, next, /*proper=*/true);
     }
@@ -394,8 +400,9 @@ class DfsRunner {
       return;
     }
     if (r >= bound_ - 1) return;
-    const Frame frame{parent, &next};
     const size_t cap = slice_cap(r);
+    if (next.size() > cap && !sorted) dev::sort_card_desc_lex(c_, next);  // slices follow the order
+    const Frame frame{parent, &next};
     for (size_t plo = 0; plo < next.size(); plo += cap) {
       recurse(next, plo, std::min(next.size(), plo + cap), r + 1, level + 1, &frame);
       if (r >= bound_ - 1) return;
