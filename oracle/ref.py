@@ -127,8 +127,19 @@ def lib():
         _dp = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
         _ip = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
         L.ref_step_costs.argtypes = [_dp, _ip, _dp, _dp, _dp, _ip, C.POINTER(C.c_int32)]
+        L.ref_run_experiment.argtypes = [_u32p, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint64,
+                                         C.c_char_p, C.c_double, C.c_uint32, C.c_int, C.c_char_p]
         _lib = L
     return _lib
+
+
+def run_experiment(ns, k, samples, seed_base, path, solver="exact", time_limit=0.0, threads=1,
+                   deterministic=True):
+    arr = np.ascontiguousarray(np.asarray(ns, np.uint32))
+    rc = lib().ref_run_experiment(arr, arr.size, k, samples, seed_base, solver.encode(), time_limit,
+                                  threads, int(deterministic), path.encode())
+    if rc != 0:
+        raise RuntimeError("reference run_experiment failed")
 
 
 def step_costs(stats, flags, tuning):

@@ -99,6 +99,28 @@ REF_API int64_t ref_power_set_oracle(uint32_t n, uint32_t k, const uint32_t* del
     return -2;
   }
 }
+// The reference's batch runner (experiment.hpp:133-188), CSV to `path`.
+REF_API int ref_run_experiment(const uint32_t* ns, size_t ns_count, uint32_t k, uint32_t samples,
+                               uint64_t seed_base, const char* solver, double time_limit,
+                               uint32_t threads, int deterministic, const char* path) {
+  try {
+    ExperimentSpec spec;
+    spec.ns.assign(ns, ns + ns_count);
+    spec.k = k;
+    spec.samples = samples;
+    spec.seed_base = seed_base;
+    spec.solver = solver;
+    spec.time_limit = time_limit > 0 ? std::optional<double>(time_limit) : std::nullopt;
+    spec.threads = threads;
+    spec.deterministic = deterministic != 0;
+    std::ofstream out(path);
+    run_experiment(spec, out, nullptr);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
 // compute_step_costs + select_step (cost_model.hpp:187-250) on a flattened
 // SearchStats; same layout as sw_step_costs in include/synchro_b200.h.
 REF_API int ref_step_costs(const double* st, const int32_t* fl, const double* tu, double* step,
