@@ -539,8 +539,9 @@ size_t hash_dedupe(Context& c, DList& l) {
   u64 slots = 1;
   while (slots < 2 * N) slots <<= 1;
   cudaStream_t s = as_stream(c.stream());
-  auto* table = static_cast<unsigned long long*>(c.alloc(slots * 8));
-  auto* slot_of = static_cast<u32*>(c.alloc(N * 4));
+  // persistent per-context scratch: no pool growth on the hot path
+  auto* table = static_cast<unsigned long long*>(c.scratch(8, slots * 8));
+  auto* slot_of = static_cast<u32*>(c.scratch(9, N * 4));
   SW_CUDA(cudaMemsetAsync(table, 0xFF, slots * 8, s));
   size_t kept = 0;
   SW_DISPATCH_W(c.W(), {
@@ -549,8 +550,6 @@ size_t hash_dedupe(Context& c, DList& l) {
     kept = run_compact<W>(c, l, KeepHashFirst{table, slot_of}, nullptr);
   });
   c.counters.kernel_launches += 2;
-  c.free(table);
-  c.free(slot_of);
   return N - kept;
 }
 
