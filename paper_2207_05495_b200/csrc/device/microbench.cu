@@ -2,6 +2,9 @@
 // "2^24 random subsets at the measured frontier density ... expanded under the
 // C3/C4 automata").  Inputs are generated on the device (SplitMix64 per set),
 // each measured call is bracketed by CUDA events on the context's stream.
+#include <algorithm>
+#include <vector>
+
 #include "dev.hpp"
 #include "kernels.cuh"
 #include "util.cuh"
@@ -64,8 +67,10 @@ double bench_expand(Context& c, u64 count, double density, u64 seed, bool invers
 double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_fraction, int iters,
                     u64* unique_out, bool lex_sort) {
   const DList src = random_sets(c, count, density, seed, dup_fraction);
-  double total = 0;
-  for (int i = 0; i <= iters; ++i) {
+  // Two warm-up calls (pool growth / first-touch mapping of the list buffers
+  // happen there), then the median of `iters` timed calls.
+  std::vector<double> ms;
+  for (int i = 0; i < iters + 2; ++i) {
     DList l = copy_list(c, src, false);
     c.sync();
     StreamTimer t(c);
@@ -74,11 +79,12 @@ double bench_dedupe(Context& c, u64 count, double density, u64 seed, double dup_
       lex_sort_dedupe(c, l);
     else
       hash_dedupe(c, l);
-    const double ms = t.stop_ms();
-    if (i > 0) total += ms;  // i == 0: warm-up
+    const double m = t.stop_ms();
+    if (i >= 2) ms.push_back(m);
     if (unique_out) *unique_out = l.size();
   }
-  return total / iters;
+  std::sort(ms.begin(), ms.end());
+  return ms[ms.size() / 2];
 }
 
 }  // namespace synchro::dev
