@@ -20,6 +20,8 @@
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
 
+#include <atomic>
+
 #include "dev.hpp"
 #include "kernels.cuh"
 #include "util.cuh"
@@ -478,14 +480,26 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   if (p.count == 0) return;
   u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..5)
   SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
-  int sms = 0, blocks_per_sm = 0, dev = 0;
-  SW_CUDA(cudaGetDevice(&dev));
-  SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  SW_DISPATCH_W(c.W(), {
-    SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
-  });
-  blocks_per_sm = std::max(1, blocks_per_sm);
+  // Persistent-grid size: queried once per (W, mode) and process (runtime
+  // queries take driver locks; many concurrent solves share the device).
+  static std::atomic<int> cache_bps[kMaxW + 1];
+  static std::atomic<int> cache_sms{0};
+  int sms = cache_sms.load(std::memory_order_relaxed);
+  if (!sms) {
+    int dev = 0;
+    SW_CUDA(cudaGetDevice(&dev));
+    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache_sms.store(sms, std::memory_order_relaxed);
+  }
+  int blocks_per_sm = cache_bps[c.W()].load(std::memory_order_relaxed);
+  if (!blocks_per_sm) {
+    SW_DISPATCH_W(c.W(), {
+      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &blocks_per_sm, contain_pool_kernel<W, PROPER, EXIST>, kPoolThreads, 0));
+    });
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    cache_bps[c.W()].store(blocks_per_sm, std::memory_order_relaxed);
+  }
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
