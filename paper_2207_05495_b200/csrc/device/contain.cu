@@ -248,7 +248,10 @@ __global__ void pad_kernel(const u64* __restrict__ src, const u32* __restrict__ 
 // query are dropped without touching global memory.
 constexpr int kPoolWarps = 6;
 constexpr int kPoolThreads = kPoolWarps * 32;
-constexpr int kPoolCap = 480;   // tasks per warp (static smem <= 48 KB per block)
+// Tasks per warp.  320 × 16 B × 6 warps = 31 KB per CTA → 5 CTAs (30 warps)
+// per SM at ~60 registers (480 gave 4 CTAs / 24 warps; ncu: latency-bound at
+// 0.7 eligible warps per scheduler).  Overflow falls back to a range scan.
+constexpr int kPoolCap = 320;
 constexpr int kPoolBrute = 16;  // ranges of <= this many keys are scanned
 constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
