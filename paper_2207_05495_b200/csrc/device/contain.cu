@@ -248,18 +248,22 @@ __global__ void pad_kernel(const u64* __restrict__ src, const u32* __restrict__ 
 // query are dropped without touching global memory.
 constexpr int kPoolWarps = 6;
 constexpr int kPoolThreads = kPoolWarps * 32;
-// Tasks per warp.  320 × 16 B × 6 warps = 31 KB per CTA → 5 CTAs (30 warps)
-// per SM at ~60 registers (480 gave 4 CTAs / 24 warps; ncu: latency-bound at
-// 0.7 eligible warps per scheduler).  Overflow falls back to a range scan.
-constexpr int kPoolCap = 320;
-constexpr int kPoolBrute = 16;  // ranges of <= this many keys are scanned
+// Tasks per warp in shared memory.  When a round would overflow the pool, its
+// bottom half (the oldest tasks) is spilled to a per-warp stack in global
+// memory and pulled back before new queries are taken; only when that stack
+// is full too does the opened range fall back to a scan.
+constexpr int kPoolCap = 256;
+constexpr int kSpill = kPoolCap / 2;
+constexpr int kSpillCap = 1024;  // tasks per warp in the global spill stack
+constexpr int kPoolBrute = 16;   // ranges of <= this many keys are scanned
 constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
 
 template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
-    u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query) {
+    u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
+    u32* overflow_scans) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
@@ -275,11 +279,24 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
   shit[lane] = kNone;
   __syncwarp();
   const u32 root_id = Na == 1 ? kLeafBit : 0u;
-  int sp = 0;
+  uint4* spill = spill_all + (static_cast<u64>(blockIdx.x) * kPoolWarps + wid) * kSpillCap;
+  int sp = 0, gsp = 0;
   bool more = true;
   while (true) {
     if (EXIST && *reinterpret_cast<volatile int*>(found)) break;
-    if (sp < 32 && more) {  // refill with fresh queries
+    if (sp < 32 && gsp > 0) {  // pull spilled tasks back first
+      const int t = gsp < kSpill ? gsp : kSpill;
+      for (int i = lane; i < t; i += 32) {
+        const uint4 v = spill[gsp - t + i];
+        sq[sp + i] = v.x;
+        sn[sp + i] = v.y;
+        sf[sp + i] = v.z;
+        sdc[sp + i] = v.w;
+      }
+      gsp -= t;
+      sp += t;
+      __syncwarp();
+    } else if (sp < 32 && more) {  // refill with fresh queries
       u32 base = 0;
       if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
       base = __shfl_sync(FULL, base, 0);
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       __syncwarp();
     }
     if (sp == 0) {
-      if (!more) break;
+      if (!more && gsp == 0) break;
       continue;
     }
     const int take = sp < 32 ? sp : 32;
@@ -392,8 +409,25 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
     const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
     const int n0 = __popc(m0), n1 = __popc(m1);
+    if (sp + n0 + n1 > kPoolCap && gsp + kSpill <= kSpillCap) {
+      // spill the oldest kSpill tasks; sp <= kPoolCap = 2 kSpill, so the
+      // shifted block [kSpill, sp) and its target [0, sp - kSpill) are disjoint
+      for (int i = lane; i < kSpill; i += 32)
+        spill[gsp + i] = make_uint4(sq[i], sn[i], sf[i], sdc[i]);
+      __syncwarp();
+      for (int i = lane; i < sp - kSpill; i += 32) {
+        sq[i] = sq[i + kSpill];
+        sn[i] = sn[i + kSpill];
+        sf[i] = sf[i + kSpill];
+        sdc[i] = sdc[i + kSpill];
+      }
+      __syncwarp();
+      gsp += kSpill;
+      sp -= kSpill;
+    }
     if (sp + n0 + n1 > kPoolCap) {
-      if (c0 != kNone) brute = true;  // pool full: scan the opened range instead
+      if (c0 != kNone) brute = true;  // pool and spill full: scan the opened range
+      if (lane == 0) atomicAdd(overflow_scans, 1u);
     } else {
       if (c1 != kNone) {
         const int pos = sp + __popc(m1 & lt);
@@ -482,7 +516,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   if (!EXIST) SW_CUDA(cudaMemsetAsync(keep, 1, Nb, s));
   if (p.count == 0) return;
   u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;  // slot 7: words 8.. (Res uses 0..5)
-  SW_CUDA(cudaMemsetAsync(counter, 0, 4, s));
+  SW_CUDA(cudaMemsetAsync(counter, 0, 8, s));  // [0] next query, [1] overflow scans
   // Persistent-grid size: queried once per (W, mode) and process (runtime
   // queries take driver locks; many concurrent solves share the device).
   static std::atomic<int> cache_bps[kMaxW + 1];
@@ -506,6 +540,8 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
+  uint4* spill = static_cast<uint4*>(
+      c.scratch(10, static_cast<size_t>(grid) * kPoolWarps * kSpillCap * sizeof(uint4)));
   std::unique_ptr<StreamTimer> timer;
   if (progress_enabled() || c.timing) {
     timer = std::make_unique<StreamTimer>(c);
@@ -514,7 +550,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
-        static_cast<u32>(Nb), keep, found, wit, counter);
+        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
@@ -525,8 +561,13 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
     c.counters.contain_ms += ms;
     c.counters.contain_launches += 1;
     c.counters.contain_bytes += (p.count + Nb) * row + (EXIST ? 0 : Nb);
-    SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms", EXIST ? "exist" : "mark",
-                     PROPER ? "-proper" : "", p.count, static_cast<unsigned long long>(Nb), ms);
+    if (progress_enabled()) {
+      u32 overflow = 0;
+      c.memcpy_d2h(&overflow, counter + 1, 4);
+      SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms overflow_scans=%u",
+                       EXIST ? "exist" : "mark", PROPER ? "-proper" : "", p.count,
+                       static_cast<unsigned long long>(Nb), ms, overflow);
+    }
   }
 }
 
@@ -626,6 +667,10 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   } else if (a.size() == 1) {
     SW_CUDA(cudaMemsetAsync(p.orig, 0, 4, s));
   }
+  if (progress_enabled()) {
+    c.sync();
+    SYNCHRO_PROGRESS("  perm-index |A|=%zu relabelled+sorted", a.size());
+  }
   p.tree = build_index(c, sorted);
   SW_DISPATCH_W(c.W(), {
     p.keys = static_cast<u64*>(c.alloc(std::max<size_t>(a.size(), 1) * Row<W>::P * 8));
@@ -635,6 +680,10 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 3;
+  if (progress_enabled()) {
+    c.sync();
+    SYNCHRO_PROGRESS("  perm-index |A|=%zu tree built", a.size());
+  }
   return p;
 }
 

@@ -140,7 +140,7 @@ class Context {
   int device_ = 0;
   void* stream_ = nullptr;
   struct Scratch { void* p = nullptr; size_t bytes = 0; };
-  Scratch scratch_[10];  // slots: kernels.cuh (8/9: hash-dedupe table, row slots)
+  Scratch scratch_[11];  // slots: kernels.cuh
 };
 
 // ---- list construction / transfer

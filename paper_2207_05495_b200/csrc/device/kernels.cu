@@ -95,8 +95,23 @@ __global__ void __launch_bounds__(256) expand_kernel(
 // of a divergent per-lane loop over set bits.  (transpose64: util.cuh)
 
 constexpr int kSliceWarps = 4;
+constexpr size_t kStageSmemLimit = 200 * 1024;
 
-template <int W, bool INV>
+// Shared memory of the sliced kernel: per warp 64W input slices + 64W output
+// slices, and (STAGED) a 64·k·W-word child block + 64·k cards; then the table.
+template <int W>
+static size_t sliced_smem(u32 k, u32 n, bool staged) {
+  size_t per_warp = 2 * 64 * W * sizeof(u64);
+  if (staged) per_warp += static_cast<size_t>(64) * k * (W * sizeof(u64) + sizeof(u32));
+  return kSliceWarps * per_warp + ((static_cast<size_t>(k) * n * 2 + 15) & ~size_t{15});
+}
+
+// STAGED: the warp's 64 parents arrive as one contiguous block (coalesced
+// 8-B loads into the staging area), and its 64·k children — contiguous in the
+// output because child o = i·k + a — leave as one block, so every global
+// access is a full-sector coalesced one.  Unstaged (large k·W only): rows are
+// read and written directly by their lanes (8-B accesses at stride 8W / 8kW).
+template <int W, bool INV, bool STAGED>
 __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
     const uint16_t* __restrict__ g_img, const u32* __restrict__ g_off,
@@ -104,12 +119,22 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     u64* __restrict__ out_tag) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 kn = k * n;
-  // [warps][64W] input slices, [warps][64W] output slices (image), table u16[k][n]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // [warps][64W] input slices, [warps][64W] output slices (image),
+  // (STAGED) [warps][64kW] child block, [warps][64k] cards; table u16[k][n]
   u64* s_slices = reinterpret_cast<u64*>(smem);
-  uint16_t* s_tab = reinterpret_cast<uint16_t*>(smem + 2 * kSliceWarps * 64 * W * sizeof(u64));
+  unsigned char* p = smem + 2 * kSliceWarps * 64 * W * sizeof(u64);
+  u64* stage = nullptr;
+  u32* scard = nullptr;
+  if (STAGED) {
+    stage = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * 64 * k * W;
+    p += static_cast<size_t>(kSliceWarps) * 64 * k * W * sizeof(u64);
+    scard = reinterpret_cast<u32*>(p) + static_cast<size_t>(wid) * 64 * k;
+    p += static_cast<size_t>(kSliceWarps) * 64 * k * sizeof(u32);
+  }
+  uint16_t* s_tab = reinterpret_cast<uint16_t*>(p);
   for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
   u64* so = s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
   const u64 batches = (count + 63) / 64;
@@ -117,11 +142,23 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
     const u64 i0 = b * 64 + lane, i1 = i0 + 32;
     const bool v0 = i0 < count, v1 = i1 < count;
+    const u32 nb = static_cast<u32>(count - b * 64 < 64 ? count - b * 64 : 64);  // parents here
+    if (STAGED) {
+      const u64* blk = src + (lo + b * 64) * W;
+      for (u32 e = lane; e < 64 * W; e += 32) stage[e] = e < nb * W ? __ldg(blk + e) : 0;
+      __syncwarp();
+    }
     // ---- parents -> slices
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const u64 r0 = v0 ? __ldg(src + (lo + i0) * W + w) : 0;
-      const u64 r1 = v1 ? __ldg(src + (lo + i1) * W + w) : 0;
+      u64 r0, r1;
+      if (STAGED) {
+        r0 = stage[lane * W + w];
+        r1 = stage[(lane + 32) * W + w];
+      } else {
+        r0 = v0 ? __ldg(src + (lo + i0) * W + w) : 0;
+        r1 = v1 ? __ldg(src + (lo + i1) * W + w) : 0;
+      }
       u64 c0, c1;
       transpose64(r0, r1, lane, c0, c1);
       sl[64 * w + lane] = c0;
@@ -153,21 +190,45 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
         }
         u64 r0, r1;
         transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
-        if (v0) out[(i0 * k + a) * W + w] = r0;
-        if (v1) out[(i1 * k + a) * W + w] = r1;
+        if (STAGED) {
+          stage[(lane * k + a) * W + w] = r0;
+          stage[((lane + 32) * k + a) * W + w] = r1;
+        } else {
+          if (v0) out[(i0 * k + a) * W + w] = r0;
+          if (v1) out[(i1 * k + a) * W + w] = r1;
+        }
         card0 += __popcll(r0);
         card1 += __popcll(r1);
       }
-      if (v0) {
-        out_card[i0 * k + a] = card0;
-        if (out_tag) out_tag[i0 * k + a] = ((lo + i0) << 16) | a;
-      }
-      if (v1) {
-        out_card[i1 * k + a] = card1;
-        if (out_tag) out_tag[i1 * k + a] = ((lo + i1) << 16) | a;
+      if (STAGED) {
+        scard[lane * k + a] = card0;
+        scard[(lane + 32) * k + a] = card1;
+      } else {
+        if (v0) {
+          out_card[i0 * k + a] = card0;
+          if (out_tag) out_tag[i0 * k + a] = ((lo + i0) << 16) | a;
+        }
+        if (v1) {
+          out_card[i1 * k + a] = card1;
+          if (out_tag) out_tag[i1 * k + a] = ((lo + i1) << 16) | a;
+        }
       }
     }
     __syncwarp();
+    if (STAGED) {  // the 64·k children of this batch are contiguous in the output
+      const u64 o0 = b * 64 * k;
+      const u32 nc = nb * k;
+      u64* dst = out + o0 * W;
+      for (u32 e = lane; e < nc * W; e += 32) dst[e] = stage[e];
+      for (u32 e = lane; e < nc; e += 32) {
+        out_card[o0 + e] = scard[e];
+        if (out_tag) {
+          const u64 o = o0 + e;
+          out_tag[o] = ((lo + o / k) << 16) | (o % k);
+        }
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -177,8 +238,6 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   out.reserve(cnt * k);
   out.set_size(cnt * k);
   if (!cnt) return;
-  const size_t kn = static_cast<size_t>(k) * n;
-  const size_t tab_bytes = kn * 2;
   cudaStream_t s = as_stream(c.stream());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.timing) {
@@ -190,8 +249,12 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   const u64 batches = (cnt + 63) / 64;
   const int grid = static_cast<int>(std::min<u64>((batches + kSliceWarps - 1) / kSliceWarps, 148 * 16));
   SW_DISPATCH_W(c.W(), {
-    const size_t shmem = 2 * kSliceWarps * 64 * W * sizeof(u64) + ((tab_bytes + 15) & ~size_t{15});
-    auto kern = inverse ? expand_sliced_kernel<W, true> : expand_sliced_kernel<W, false>;
+    const bool staged = sliced_smem<W>(k, n, true) <= kStageSmemLimit;
+    const size_t shmem = sliced_smem<W>(k, n, staged);
+    auto kern = staged ? (inverse ? expand_sliced_kernel<W, true, true>
+                                  : expand_sliced_kernel<W, false, true>)
+                       : (inverse ? expand_sliced_kernel<W, true, false>
+                                  : expand_sliced_kernel<W, false, false>);
     if (shmem > 48 * 1024)
       SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(shmem)));

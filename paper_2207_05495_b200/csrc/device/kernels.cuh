@@ -2,7 +2,8 @@
 //
 // Scratch-slot convention (Context::scratch): 0/1 sort keys, 2/3 sort
 // permutations, 4 CUB temp storage, 5 flag arrays, 6 compaction tile counts,
-// 7 small reductions / result words.
+// 7 small reductions / result words, 8/9 hash-dedupe table and row slots,
+// 10 containment-traversal spill stacks.
 #pragma once
 
 #include <cstdint>

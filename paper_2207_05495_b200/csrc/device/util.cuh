@@ -61,17 +61,30 @@ __device__ __forceinline__ u64 range_mask(int w, int s, int e) {
 
 // 32x32 bit transposes of the two 32-bit halves of x across the warp (row =
 // lane, MSB-first columns), by five stages of recursive block swaps.
+//
+// Stage j pairs lane l with l^j: the lane with bit j clear keeps x & ~m and
+// needs its partner's (x & ~m) >> j; the lane with bit j set keeps x & m and
+// needs (x & m) << j.  So each lane pre-shifts exactly the half its partner
+// needs and ships only that: mask, 32-bit rotate (no bits wrap — the masks
+// are zero where a rotate would wrap), one shuffle, merge = 4 instructions
+// per 32-bit word per stage.
+__device__ __forceinline__ u32 rotl32(u32 x, u32 r) { return __funnelshift_l(x, x, r); }
+
 __device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
-  constexpr u64 kM[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
-                         0x3333333333333333ull, 0x5555555555555555ull};
+  constexpr u32 kM[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+  u32 hi = static_cast<u32>(x >> 32), lo = static_cast<u32>(x);
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const int j = 16 >> s;
-    const u64 m = kM[s];
-    const u64 y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
-    x = (lane & j) ? ((x & m) | ((y & m) << j)) : ((x & ~m) | ((y & ~m) >> j));
+    const bool up = (lane & j) != 0;
+    const u32 keep = up ? kM[s] : ~kM[s];
+    const u32 rot = up ? 32 - j : j;
+    const u32 sh = __shfl_xor_sync(0xFFFFFFFFu, rotl32(hi & ~keep, rot), j);
+    const u32 sl = __shfl_xor_sync(0xFFFFFFFFu, rotl32(lo & ~keep, rot), j);
+    hi = (hi & keep) | sh;
+    lo = (lo & keep) | sl;
   }
-  return x;
+  return (static_cast<u64>(hi) << 32) | lo;
 }
 
 // 64x64 bit transpose across a warp: lane l holds rows l and l+32 (r0, r1)
