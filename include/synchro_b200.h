@@ -164,6 +164,12 @@ int sw_list_sort_card_desc_lex(uint32_t n, uint64_t* words, uint32_t* cards, uin
                                size_t count);
 int sw_list_dedupe_sorted(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
                           size_t count, size_t* out_count);
+/* Set-semantics dedupe (the surviving set of lex_sort_dedupe, set_list.hpp:
+ * 259-265, without the sort): one row per distinct value, survivors in
+ * unspecified order.  With tags, each survivor carries the tag of the value's
+ * first occurrence (the reference's survivor).  In place; tags may be NULL. */
+int sw_list_hash_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                        size_t count, size_t* out_count);
 int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards, size_t count,
                                 size_t* out_count);
 /* keep[j] = 1 iff b[j] is NOT marked.  mode 0: supersets (incl. equal),

@@ -375,6 +375,12 @@ SW_EXPORT int sw_list_dedupe_sorted(uint32_t n, uint64_t* words, uint32_t* cards
                  [](dev::Context& c, dev::DList& l) { dev::dedupe_sorted(c, l); });
 }
 
+SW_EXPORT int sw_list_hash_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* tags,
+                                  size_t count, size_t* out_count) {
+  return list_op(n, words, cards, tags, count, out_count,
+                 [](dev::Context& c, dev::DList& l) { dev::hash_dedupe(c, l); });
+}
+
 SW_EXPORT int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards,
                                           size_t count, size_t* out_count) {
   if (!sorted_unique(words, count, words_for(n))) {

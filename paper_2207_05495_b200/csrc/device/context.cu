@@ -44,6 +44,12 @@ Context::Context(const Automaton& aut, int device)
   SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
   u64 thresh = ~u64{0};
   SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  // L2 set-aside for persisting accesses (the dedupe hash table is marked
+  // persisting while the rows stream past it; unused set-aside stays
+  // available to normal accesses).
+  int carve = 0;
+  SW_CUDA(cudaDeviceGetAttribute(&carve, cudaDevAttrMaxPersistingL2CacheSize, device_));
+  if (carve > 0) SW_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(carve)));
 
   // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
   const InverseTransitions inv(aut);

@@ -163,8 +163,10 @@ void sort_lex(Context& c, DList& l);                   // stable, index tie-brea
 void sort_card_desc_lex(Context& c, DList& l);         // card desc, lex, index
 size_t dedupe_sorted(Context& c, DList& l);            // returns #removed
 size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
-// Set-semantics dedupe by open-addressing hash: keeps the first occurrence of
-// every distinct row, survivors in their original order.  Returns #removed.
+// Set-semantics dedupe by open-addressing hash (dedupe.cu): one row per
+// distinct value, survivors in UNSPECIFIED order (callers are order-free).
+// Tagged lists keep the first occurrence's tag (minimum index, the
+// reference's survivor).  Returns #removed.
 size_t hash_dedupe(Context& c, DList& l);
 
 // ---- containment (subset_algebra.hpp:138-231, static_trie.hpp:51-55)

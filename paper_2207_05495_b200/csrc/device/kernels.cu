@@ -172,9 +172,13 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
 #pragma unroll
         for (int i = 0; i < 2 * W; ++i) so[32 * i + lane] = 0;
         __syncwarp();
-        for (u32 q = lane; q < n; q += 32)
-          atomicOr(reinterpret_cast<unsigned long long*>(&so[s_tab[base + q]]),
-                   static_cast<unsigned long long>(sl[q]));
+        // two native 32-bit ORs (a 64-bit shared atomicOr is a CAS spin loop)
+        for (u32 q = lane; q < n; q += 32) {
+          const u64 v = sl[q];
+          u32* dst = reinterpret_cast<u32*>(&so[s_tab[base + q]]);
+          if (static_cast<u32>(v)) atomicOr(dst, static_cast<u32>(v));
+          if (v >> 32) atomicOr(dst + 1, static_cast<u32>(v >> 32));
+        }
         __syncwarp();
       }
 #pragma unroll
@@ -595,7 +599,7 @@ struct KeepHashFirst {
   }
 };
 
-size_t hash_dedupe(Context& c, DList& l) {
+size_t hash_dedupe_wide(Context& c, DList& l) {
   const u64 N = l.size();
   if (N <= 1) return 0;
   if (N >= 0xFFFFFFFFull) throw std::invalid_argument("hash_dedupe: list too large");

@@ -18,6 +18,10 @@ size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm)
 // Keep the first row of every run of equal rows in perm order (sorted input).
 size_t compact_unique(Context& c, DList& l, const u32* perm);
 
+// Hash dedupe with a 64-bit (tag << 32 | index) table, for lists whose indices
+// exceed the 25 bits of dedupe.cu's compact entries.
+size_t hash_dedupe_wide(Context& c, DList& l);
+
 // hist[q] = number of sets of l containing state q (q < n); hist is a device
 // array of n u32, overwritten.  Bit-sliced: 64 sets per warp transpose.
 void state_histogram(Context& c, const DList& l, u32* hist);

@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = [
     "sw_power_set_oracle", "sw_engine_create", "sw_engine_destroy", "sw_engine_choose",
     "sw_engine_step", "sw_engine_meet", "sw_engine_dfs", "sw_engine_stats_get",
     "sw_list_expand", "sw_list_lex_sort_dedupe", "sw_list_sort_card_desc_lex",
-    "sw_list_dedupe_sorted", "sw_list_self_reduce_minimal", "sw_list_mark",
+    "sw_list_dedupe_sorted", "sw_list_hash_dedupe", "sw_list_self_reduce_minimal", "sw_list_mark",
     "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
     "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe",
 ]
@@ -147,6 +147,8 @@ def load():
     L.sw_list_sort_card_desc_lex.argtypes = [C.c_uint32, _u64p, _u32p, C.c_void_p, C.c_size_t]
     L.sw_list_dedupe_sorted.argtypes = [C.c_uint32, _u64p, _u32p, C.c_void_p, C.c_size_t,
                                         C.POINTER(C.c_size_t)]
+    L.sw_list_hash_dedupe.argtypes = [C.c_uint32, _u64p, _u32p, C.c_void_p, C.c_size_t,
+                                      C.POINTER(C.c_size_t)]
     L.sw_list_self_reduce_minimal.argtypes = [C.c_uint32, _u64p, _u32p, C.c_size_t,
                                               C.POINTER(C.c_size_t)]
     L.sw_list_mark.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t, C.c_int32, _u8p]
@@ -471,6 +473,17 @@ def list_dedupe_sorted(n: int, words: np.ndarray, tags: Optional[np.ndarray] = N
     t = None if tags is None else np.array(tags, np.uint64).copy()
     out = C.c_size_t()
     _check(load().sw_list_dedupe_sorted(n, w, c, _tags_ptr(t), c.size, C.byref(out)))
+    m = out.value
+    return w[: m * W(n)], c[:m], (t[:m] if t is not None else None)
+
+
+def list_hash_dedupe(n: int, words: np.ndarray, tags: Optional[np.ndarray] = None):
+    """First occurrence of every distinct row, original order (GPU hash dedupe)."""
+    w = np.array(words, np.uint64).copy()
+    c = cards_of(n, w)
+    t = None if tags is None else np.array(tags, np.uint64).copy()
+    out = C.c_size_t()
+    _check(load().sw_list_hash_dedupe(n, w, c, _tags_ptr(t), c.size, C.byref(out)))
     m = out.value
     return w[: m * W(n)], c[:m], (t[:m] if t is not None else None)
 

@@ -9,7 +9,7 @@ from paper_2207_05495_b200 import native as sw  # noqa: E402
 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json"))).get("hbm_gbs", 6554.6)
-count = 1 << 24
+count = 1 << int(os.environ.get("MICRO_LOG2", "24"))
 for spec in sys.argv[1:] or ["random:300,2,0"]:
     aut = sw.from_spec(spec)
     W = (aut.n + 63) // 64

@@ -42,6 +42,73 @@ def test_lex_sort_dedupe(gpu, ref, n, density):
     assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
 
 
+def _first_occurrence(n, words):
+    seen, keep = set(), []
+    for i, r in enumerate(rows(n, words)):
+        if r not in seen:
+            seen.add(r)
+            keep.append(i)
+    return np.array(keep, dtype=np.int64)
+
+
+def _as_set(n, words, cards, tags=None):
+    rs = rows(n, words)
+    return sorted(zip(rs, cards.tolist(), tags.tolist() if tags is not None else [0] * len(rs)))
+
+
+@pytest.mark.parametrize("n,density", SHAPES)
+@pytest.mark.parametrize("count", [1, 2, 127, 128, 129, 513, 7000])
+def test_hash_dedupe_first_occurrence(gpu, n, density, count):
+    """Tagged: the survivors are the first occurrences (row, card, tag) — the
+    set lex_sort_dedupe keeps; order unspecified."""
+    rng = np.random.default_rng(count + n)
+    base = random_list(n, max(1, count // 2), density, 11).reshape(-1, W(n))
+    pick = rng.integers(0, base.shape[0], size=count)  # ~half duplicates, scattered
+    words = base[pick].reshape(-1)
+    tags = rng.integers(0, 2**48, size=count, dtype=np.uint64)
+    keep = _first_occurrence(n, words)
+    kw = words.reshape(-1, W(n))[keep].reshape(-1)
+    gw, gc, gt = gpu.list_hash_dedupe(n, words, tags)
+    assert _as_set(n, gw, gc, gt) == _as_set(n, kw, gpu.cards_of(n, kw), tags[keep])
+
+
+@pytest.mark.parametrize("n,density", SHAPES)
+@pytest.mark.parametrize("count", [1, 129, 7000])
+def test_hash_dedupe_untagged(gpu, n, density, count):
+    rng = np.random.default_rng(count * 3 + n)
+    base = random_list(n, max(1, count // 2), density, 13).reshape(-1, W(n))
+    words = base[rng.integers(0, base.shape[0], size=count)].reshape(-1)
+    gw, gc, _ = gpu.list_hash_dedupe(n, words)
+    out = rows(n, gw)
+    assert len(out) == len(set(out)) and set(out) == set(rows(n, words))
+    assert np.array_equal(gc, gpu.cards_of(n, gw))
+
+
+@pytest.mark.parametrize("tagged", [False, True])
+def test_hash_dedupe_long_probe_chains(gpu, monkeypatch, tagged):
+    """A table packed to N+64 slots: long probe chains (past the one-byte probe
+    distance of the tagged path's resolve kernel); survivors must not change."""
+    monkeypatch.setenv("SYNCHRO_DEDUPE_FULL_TABLE", "1")
+    n = 100
+    base = random_list(n, 30000, 0.1, 12).reshape(-1, W(n))
+    pick = np.random.default_rng(5).integers(0, base.shape[0], size=40000)
+    words = base[pick].reshape(-1)
+    keep = _first_occurrence(n, words)
+    kw = words.reshape(-1, W(n))[keep].reshape(-1)
+    if tagged:
+        tags = np.arange(40000, dtype=np.uint64)
+        gw, gc, gt = gpu.list_hash_dedupe(n, words, tags)
+        assert _as_set(n, gw, gc, gt) == _as_set(n, kw, gpu.cards_of(n, kw), tags[keep])
+    else:
+        gw, gc, _ = gpu.list_hash_dedupe(n, words)
+        assert _as_set(n, gw, gc) == _as_set(n, kw, gpu.cards_of(n, kw))
+
+
+def test_hash_dedupe_empty(gpu):
+    gw, gc, _ = gpu.list_hash_dedupe(100, np.zeros(0, np.uint64))
+    assert gw.size == 0 and gc.size == 0
+
+
 @pytest.mark.parametrize("n,density", SHAPES)
 def test_sort_card_desc_lex_and_dedupe(gpu, ref, n, density):
     base = random_list(n, 2000, density, 9)
