@@ -288,8 +288,9 @@ def run_ours(args, world, rank, local):
                             "ms_per_launch": mb_exp_ms, "children_per_launch": mb_count * aut.k,
                             "in_engine_achieved": achieved,
                             "in_engine_share_of_step": exp_ms / engine_ms if engine_ms else None},
-        "roofline_dedupe": {"bound": "hbm", "kernel": "hash_insert_kernel + fused warp-ballot "
-                                                       "compaction (phase-1 frontier dedupe)",
+        "roofline_dedupe": {"bound": "hbm", "kernel": "dd_single_kernel (one pass: hash claim in a "
+                                                       "32-bit L2-sized table + warp-tile block "
+                                                       "reservation; untagged frontier dedupe)",
                             "achieved": dd_gbs, "peak": roof_peak, "unit": "GB/s",
                             "frac": dd_gbs / roof_peak, "ms_per_call": dd_ms,
                             "sets": mb_count, "unique": dd_unique,

@@ -312,14 +312,55 @@ __global__ void __launch_bounds__(kDdThreads) dd_resolve_kernel(
   }
 }
 
+// One row's claim after its optimistic CAS at home found `c` != 0: walk the
+// chain one 32-byte sector (8 slots) per L2 round trip, decoding each sector
+// into empty / tag-match bit masks; CAS only into empty slots.  Returns true
+// if `mine` claimed a slot, false if an equal row holds one.
+template <int W>
+__device__ __forceinline__ bool claim_one(u32* table, u32 nslots, const u64* __restrict__ words,
+                                          const u64* row, u32 home, u32 mine, u32 c) {
+  const u32 tg = mine >> kIdxBits;
+  if ((c >> kIdxBits) == tg && row_equal<W>(words, (c & kIdxMask) - 1, row)) return false;
+  u32 s = home + 1 == nslots ? 0 : home + 1;
+  while (true) {
+    const u32 g = s & ~7u;  // nslots is a multiple of 8
+    const uint4 qa = __ldcg(reinterpret_cast<const uint4*>(table + g));
+    const uint4 qb = __ldcg(reinterpret_cast<const uint4*>(table + g + 4));
+    const u32 e[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+    u32 E = 0, M = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      E |= static_cast<u32>(e[k] == 0) << k;
+      M |= static_cast<u32>((e[k] >> kIdxBits) == tg && e[k] != 0) << k;
+    }
+    u32 m = (E | M) & (0xFFu << (s - g)) & 0xFFu;
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      u32 v = e[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) v = q == k ? e[q] : v;
+      if ((E >> k) & 1) {
+        v = atomicCAS(&table[g + k], 0u, mine);
+        if (v == 0) return true;
+      }
+      if ((v >> kIdxBits) == tg && row_equal<W>(words, (v & kIdxMask) - 1, row)) return false;
+    }
+    s = g + 8 >= nslots ? 0 : g + 8;
+  }
+}
+
 // Untagged lists: equal rows are indistinguishable, so the survivor of a
 // group is simply whichever occurrence claims the slot first — one pass.
-// The unit of work is a WARP tile of 32·R rows with no block barriers: the
-// warp stages its rows (coalesced), hashes and claims them (all R claims in
-// flight), finds its output offset by decoupled look-back over warp tiles,
-// and writes its survivors as one contiguous block.  Warps never wait for
-// each other except through the look-back, so probe chains and L2/HBM
-// latency of one warp overlap with the others.  Rows are read once.
+// The unit of work is a WARP tile of 32·R rows with no block barriers:
+//   A  rows staged in shared memory (coalesced); each lane hashes its R rows
+//      and issues their optimistic claims (CAS at home) before using any
+//      result; rows whose home was taken go to a warp-compacted pending list;
+//   B  the whole warp walks the pending chains, one row per lane (rows re-read
+//      from shared memory — no per-lane row state is carried across phases);
+//   C  survivors reserve an output block with one atomicAdd per warp (set
+//      semantics: their order is unspecified) and leave as one block.
+// Rows are read from HBM once.
 template <int W>
 __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
     const u64* __restrict__ words, const u32* __restrict__ cards, u64 N, u32* table, u32 nslots,
@@ -328,8 +369,16 @@ __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
   constexpr int R = rows_per_thread<W>(), T = 32 * R;
   extern __shared__ __align__(16) u64 smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u64* srow = smem + static_cast<size_t>(wid) * (T * W + T / 2);
+  // per warp: rows T*W u64 | cards T u32 | home T u32 | cur T u32 | mine T u32 | pending T u16 | keep T u8
+  constexpr int kWarpBytes = T * W * 8 + T * 4 * 4 + T * 2 + T;
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wid) * ((kWarpBytes + 15) & ~15);
+  u64* srow = reinterpret_cast<u64*>(wbase);
   u32* scard = reinterpret_cast<u32*>(srow + T * W);
+  u32* shome = scard + T;
+  u32* scur = shome + T;
+  u32* smine = scur + T;
+  uint16_t* spend = reinterpret_cast<uint16_t*>(smine + T);
+  uint8_t* skeep = reinterpret_cast<uint8_t*>(spend + T);
   const u64 ntiles = (N + T - 1) / T;
   const unsigned lt = (1u << lane) - 1;
   while (true) {
@@ -342,39 +391,60 @@ __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
     const u64* src = words + base * W;
     for (u32 e = lane; e < cnt * W; e += 32) srow[e] = __ldcs(src + e);
     __syncwarp();
+    // ---- A: hash + optimistic claims, all R in flight
+    u32 cur[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const u32 r = j * 32 + lane;
+      u64 row[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) row[w] = srow[r * W + w];
+      const u64 h = row_hash<W>(row);
+      const u32 home = home_slot(h, nslots);
+      const u32 mine = (tag7(h) << kIdxBits) | static_cast<u32>(base + r + 1);
+      shome[r] = home;
+      smine[r] = mine;
+      cur[j] = r < cnt ? atomicCAS(&table[home], 0u, mine) : 0u;
+    }
+    u32 npend = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const u32 r = j * 32 + lane;
+      const bool pend = r < cnt && cur[j] != 0;
+      skeep[r] = r < cnt && cur[j] == 0;
+      scur[r] = cur[j];
+      const unsigned b = __ballot_sync(0xFFFFFFFFu, pend);
+      if (pend) spend[npend + __popc(b & lt)] = static_cast<uint16_t>(r);
+      npend += __popc(b);
+    }
+    __syncwarp();
+    // ---- B: pending chains, one row per lane
+    for (u32 p = lane; p < npend; p += 32) {
+      const u32 r = spend[p];
+      u64 row[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) row[w] = srow[r * W + w];
+      skeep[r] = claim_one<W>(table, nslots, words, row, shome[r], smine[r], scur[r]);
+    }
+    __syncwarp();
+    // ---- C: reserve and write the survivors
     u64 row[R][W];
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const u32 r = j * 32 + lane;
-#pragma unroll
-      for (int w = 0; w < W; ++w) row[j][w] = r < cnt ? srow[r * W + w] : 0;
-    }
-    u32 s[R], mine[R], cur[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) {  // all claims in flight before any result is used
-      const u32 r = j * 32 + lane;
-      const u64 h = row_hash<W>(row[j]);
-      s[j] = home_slot(h, nslots);
-      mine[j] = (tag7(h) << kIdxBits) | static_cast<u32>(base + r + 1);
-      cur[j] = r < cnt ? atomicCAS(&table[s[j]], 0u, mine[j]) : 1u;
-    }
-    bool keep[R], valid[R];
-    u32 sl[R], d[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) valid[j] = j * 32 + lane < cnt;
-    claim_rows<W, R>(table, nslots, words, row, s, mine, cur, valid, keep, sl, d);
-    u32 agg = 0;
+    bool keep[R];
     unsigned bal[R];
+    u32 agg = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
+      const u32 r = j * 32 + lane;
+      keep[j] = skeep[r] != 0;
       bal[j] = __ballot_sync(0xFFFFFFFFu, keep[j]);
       agg += __popc(bal[j]);
+#pragma unroll
+      for (int w = 0; w < W; ++w) row[j][w] = keep[j] ? srow[r * W + w] : 0;
     }
-    // reserve the output block (set semantics: survivors' order is unspecified)
     u64 excl = 0;
     if (lane == 0 && agg) excl = atomicAdd(out_count, static_cast<unsigned long long>(agg));
     excl = __shfl_sync(0xFFFFFFFFu, excl, 0);
-    // compact into the warp's staging rows (all lanes have their rows in registers)
+    __syncwarp();
     u32 off = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -392,6 +462,12 @@ __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
     for (u32 e = lane; e < agg; e += 32) __stcs(oc + excl + e, scard[e]);
     __syncwarp();
   }
+}
+
+template <int W>
+constexpr size_t single_warp_bytes() {
+  constexpr int T = 32 * rows_per_thread<W>();
+  return (static_cast<size_t>(T) * W * 8 + T * 4 * 4 + T * 2 + T + 15) & ~size_t{15};
 }
 
 // Marks [p, p+bytes) persisting in L2 for kernels on stream s while alive
@@ -445,7 +521,7 @@ static size_t hash_dedupe_single(Context& c, DList& l) {
   auto* aux = static_cast<u64*>(c.scratch(6, 16));  // [tile counter, output count]
   SW_CUDA(cudaMemsetAsync(table, 0, static_cast<size_t>(nslots) * 4, s));
   SW_CUDA(cudaMemsetAsync(aux, 0, 16, s));
-  const size_t smem = static_cast<size_t>(kDdThreads / 32) * (T * W * 8 + T * 4);
+  const size_t smem = static_cast<size_t>(kDdThreads / 32) * single_warp_bytes<W>();
   SW_CUDA(cudaFuncSetAttribute(dd_single_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   DList out(&c, N, false);
