@@ -339,24 +339,35 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u32 limit = PROPER ? cy - 1 : cy;
     const bool is_leaf = (id & kLeafBit) != 0;
 
-    // ---- one concurrent round of loads
+    // ---- one concurrent round of loads.  A leaf needs its key row and the
+    // whole query row; an internal node only the node and the query's words
+    // d/64 and d/64+1: with need = lcp - d <= 64 the unchecked prefix bits
+    // [d, lcp) and the split bit lcp all lie in them (bits below d are
+    // masked).  Brute ranges and longer runs fetch the whole row in round 2.
     u64 y[W], xf[W];
     u32 ycard = 0, kcard = 0;
+    u64 ya = 0, yb = 0;
+    const int q0 = d >> 6;
     Node nd{};
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
     if (have) {
-      // a node visit needs the node (its window covers the prefix check) and y;
-      // only a leaf (single key) needs the key row itself
-      load_row<W>(B, j, y, ycard);
-      if (is_leaf) load_row<W>(A, first, xf, kcard);
-      else nd = nodes[id];
+      if (is_leaf) {
+        load_row<W>(B, j, y, ycard);
+        load_row<W>(A, first, xf, kcard);
+      } else {
+        nd = nodes[id];
+        const u64* yr = B + static_cast<u64>(j) * Row<W>::P;
+        ya = __ldg(yr + q0);
+        yb = q0 + 1 < W ? __ldg(yr + q0 + 1) : 0;
+      }
     }
+    auto yword = [&](int q) { return q == q0 ? ya : (q == q0 + 1 ? yb : u64{0}); };
 
     // ---- evaluate the task
-    bool hit = false, brute = false;
+    bool hit = false, brute = false, longrun = false;
     u32 hit_a = 0, c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
-    int dchild = 0;
+    int dchild = 0, L = 0;
     if (have) {
       if (is_leaf) {
         if (kcard <= limit && is_subset<W>(xf, y)) {
@@ -369,38 +380,54 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
           bf = nd.first;
           bl = nd.last;
         } else {
-          const int L = nd.lcp;
+          L = nd.lcp;
           const int need = L - d;  // common-prefix bits not yet checked
-          u64 bad = 0;
-          if (need > 0 && need <= 64) {
-            const u64 yw = window_before(
-                [&](int q) {
-                  u64 v = 0;
-#pragma unroll
-                  for (int w = 0; w < W; ++w) v = (w == q) ? y[w] : v;
-                  return v;
-                },
-                L);
-            const u64 m = need == 64 ? ~u64{0} : ((u64{1} << need) - 1);
-            bad = nd.window & ~yw & m;
-          } else if (need > 64) {  // long common run: check against the key row
-            u32 kc;
-            load_row<W>(A, nd.first, xf, kc);
-#pragma unroll
-            for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
-          }
-          if (!bad) {
-            c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
-            f0 = nd.first;
-            if ((y[L >> 6] >> (63 - (L & 63))) & 1) {
-              c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
-              f1 = nd.split + 1;
+          if (need > 64) {
+            longrun = true;  // checked against the key row in round 2
+          } else {
+            u64 bad = 0;
+            if (need > 0) {
+              const u64 yw = window_before(yword, L);
+              const u64 m = need == 64 ? ~u64{0} : ((u64{1} << need) - 1);
+              bad = nd.window & ~yw & m;
             }
-            dchild = L + 1;
-            bf = nd.first;
-            bl = nd.last;
+            if (!bad) {
+              c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+              f0 = nd.first;
+              if ((yword(L >> 6) >> (63 - (L & 63))) & 1) {
+                c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+                f1 = nd.split + 1;
+              }
+              dchild = L + 1;
+              bf = nd.first;
+              bl = nd.last;
+            }
           }
         }
+      }
+    }
+    // ---- round 2: whole query rows for brute ranges (their owner's row is
+    // shuffled to the scanning lanes) and long common runs
+    if (brute || longrun) load_row<W>(B, j, y, ycard);
+    if (longrun) {
+      u32 kc;
+      load_row<W>(A, nd.first, xf, kc);
+      u64 bad = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
+      if (!bad) {
+        u64 yl = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) yl = (w == (L >> 6)) ? y[w] : yl;
+        c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
+        f0 = nd.first;
+        if ((yl >> (63 - (L & 63))) & 1) {
+          c1 = nd.split + 1 == nd.last ? (kLeafBit | nd.last) : nd.split + 1;
+          f1 = nd.split + 1;
+        }
+        dchild = L + 1;
+        bf = nd.first;
+        bl = nd.last;
       }
     }
 
