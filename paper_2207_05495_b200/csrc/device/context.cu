@@ -44,12 +44,6 @@ Context::Context(const Automaton& aut, int device)
   SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
   u64 thresh = ~u64{0};
   SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
-  // L2 set-aside for persisting accesses (the dedupe hash table is marked
-  // persisting while the rows stream past it; unused set-aside stays
-  // available to normal accesses).
-  int carve = 0;
-  SW_CUDA(cudaDeviceGetAttribute(&carve, cudaDevAttrMaxPersistingL2CacheSize, device_));
-  if (carve > 0) SW_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(carve)));
 
   // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
   const InverseTransitions inv(aut);
@@ -259,6 +253,24 @@ DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged) 
     SW_CUDA(cudaMemcpyAsync(out.words, l.words + lo * c.W(), cnt * c.W() * 8, cudaMemcpyDeviceToDevice, s));
     SW_CUDA(cudaMemcpyAsync(out.cards, l.cards + lo, cnt * 4, cudaMemcpyDeviceToDevice, s));
     if (out.tagged()) SW_CUDA(cudaMemcpyAsync(out.tags, l.tags + lo, cnt * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  out.set_size(cnt);
+  return out;
+}
+
+DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool tagged) {
+  const size_t cnt = start < l.size() ? (l.size() - start + stride - 1) / stride : 0;
+  DList out(&c, cnt, tagged && l.tagged());
+  cudaStream_t s = as_stream(c.stream());
+  if (cnt) {  // rows i = start + j*stride: 2D copies with a source pitch of stride rows
+    const size_t row = static_cast<size_t>(c.W()) * 8;
+    SW_CUDA(cudaMemcpy2DAsync(out.words, row, l.words + start * c.W(), row * stride, row, cnt,
+                              cudaMemcpyDeviceToDevice, s));
+    SW_CUDA(cudaMemcpy2DAsync(out.cards, 4, l.cards + start, 4 * stride, 4, cnt,
+                              cudaMemcpyDeviceToDevice, s));
+    if (out.tagged())
+      SW_CUDA(cudaMemcpy2DAsync(out.tags, 8, l.tags + start, 8 * stride, 8, cnt,
+                                cudaMemcpyDeviceToDevice, s));
   }
   out.set_size(cnt);
   return out;

@@ -470,41 +470,6 @@ constexpr size_t single_warp_bytes() {
   return (static_cast<size_t>(T) * W * 8 + T * 4 * 4 + T * 2 + T + 15) & ~size_t{15};
 }
 
-// Marks [p, p+bytes) persisting in L2 for kernels on stream s while alive
-// (the table is hit at random by every row; the rows stream past it with
-// evict-first loads/stores).  Uses the carve-out Context sets at creation.
-class PersistWindow {
- public:
-  PersistWindow(cudaStream_t s, void* p, size_t bytes) : s_(s) {
-    int dev = 0, max_win = 0, carve = 0;
-    SW_CUDA(cudaGetDevice(&dev));
-    SW_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-    SW_CUDA(cudaDeviceGetAttribute(&carve, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    if (max_win <= 0 || carve <= 0) return;
-    cudaStreamAttrValue v{};
-    v.accessPolicyWindow.base_ptr = p;
-    v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, static_cast<size_t>(max_win));
-    v.accessPolicyWindow.hitRatio =
-        std::min(1.0f, static_cast<float>(carve) / static_cast<float>(v.accessPolicyWindow.num_bytes));
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    SW_CUDA(cudaStreamSetAttribute(s_, cudaStreamAttributeAccessPolicyWindow, &v));
-    on_ = true;
-  }
-  ~PersistWindow() {
-    if (!on_) return;
-    cudaStreamAttrValue v{};
-    v.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(s_, cudaStreamAttributeAccessPolicyWindow, &v);
-  }
-  PersistWindow(const PersistWindow&) = delete;
-  PersistWindow& operator=(const PersistWindow&) = delete;
-
- private:
-  cudaStream_t s_;
-  bool on_ = false;
-};
-
 }  // namespace
 
 template <int W>
@@ -527,7 +492,6 @@ static size_t hash_dedupe_single(Context& c, DList& l) {
   DList out(&c, N, false);
   const unsigned grid = static_cast<unsigned>(
       std::min<u64>((ntiles + kDdThreads / 32 - 1) / (kDdThreads / 32), 148 * 8));
-  PersistWindow pw(s, table, static_cast<size_t>(nslots) * 4);
   dd_single_kernel<W><<<grid, kDdThreads, smem, s>>>(
       l.words, l.cards, N, table, nslots, reinterpret_cast<u32*>(aux), out.words, out.cards,
       reinterpret_cast<unsigned long long*>(aux + 1));
@@ -535,7 +499,6 @@ static size_t hash_dedupe_single(Context& c, DList& l) {
   c.counters.kernel_launches += 1;
   u64 kept = 0;
   c.memcpy_d2h(&kept, aux + 1, 8);
-  cudaCtxResetPersistingL2Cache();  // release the table's lines for other work
   out.set_size(kept);
   l = std::move(out);
   return N - kept;
@@ -563,7 +526,6 @@ static size_t hash_dedupe_tiled(Context& c, DList& l) {
   const u64 per_pass = static_cast<u64>(kDdThreads) * rows_per_thread<W>();
   const unsigned grid_ins =
       static_cast<unsigned>(std::max<u64>(1, std::min<u64>((N + per_pass - 1) / per_pass, 148 * 8)));
-  PersistWindow pw(s, table, static_cast<size_t>(nslots) * 4);
   dd_insert_kernel<W><<<grid_ins, kDdThreads, 0, s>>>(l.words, N, table, nslots, dist);
   SW_CHECK_LAUNCH();
   DList out(&c, N, true);
@@ -576,7 +538,6 @@ static size_t hash_dedupe_tiled(Context& c, DList& l) {
   c.counters.kernel_launches += 2;
   u64 kept = 0;
   c.memcpy_d2h(&kept, aux + 1, 8);
-  cudaCtxResetPersistingL2Cache();
   out.set_size(kept);
   l = std::move(out);
   return N - kept;

@@ -218,6 +218,8 @@ void keep_card_at_most(Context& c, DList& l, u32 max_card);
 void keep_card_at_least(Context& c, DList& l, u32 min_card);  // plain card of complements
 void truncate(DList& l, size_t count);
 DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged);
+// Rows start, start+stride, start+2·stride, ... (2D copies; no kernel).
+DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool tagged);
 // h := sorted merge of disjoint lex-sorted unique lists h and add (untagged).
 void merge_sorted(Context& c, DList& h, const DList& add);
 u64 read_tag(Context& c, const DList& l, size_t i);

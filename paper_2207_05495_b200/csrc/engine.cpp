@@ -321,17 +321,24 @@ class DfsRunner {
       : c_(c), lbfs_(lbfs), index_(index), ledger_(ledger), t_(t), deadline_(deadline),
         tracking_(tracking), log_(log) {}
 
-  // Shard s of c explores the subtrees of initial[begin, end) only, with
-  // [begin, end) the s-th of c contiguous, equal shares (c = 1: everything).
+  // Shard s of c explores the subtrees of initial[i] for i ≡ s (mod c) only
+  // (c = 1: everything).  Interleaved rather than contiguous shares: the work
+  // below an initial set falls with its position in L_IBFS's order (n=570 s0,
+  // 8 contiguous shares: 174 s down to 56 s per shard).
   u64 run(const DList& initial, u64 r0, u64 bound, u32 shard = 0, u32 shards = 1) {
     bound_ = bound;
     if (r0 >= bound_ || initial.empty()) return bound_;
-    const size_t per = (initial.size() + shards - 1) / shards;
-    const size_t begin = std::min(initial.size(), static_cast<size_t>(shard) * per);
-    const size_t end = std::min(initial.size(), begin + per);
+    DList share;
+    const DList* roots = &initial;
+    if (shards > 1) {
+      share = dev::strided_copy(c_, initial, shard, shards, tracking_);
+      roots = &share;
+      root_start_ = shard;
+      root_stride_ = shards;
+    }
     const size_t cap = slice_cap(r0 - 1);
-    for (size_t lo = begin; lo < end; lo += cap) {
-      recurse(initial, lo, std::min(end, lo + cap), r0, 0, nullptr);
+    for (size_t lo = 0; lo < roots->size(); lo += cap) {
+      recurse(*roots, lo, std::min(roots->size(), lo + cap), r0, 0, nullptr);
       if (r0 >= bound_) break;
     }
     return bound_;
@@ -417,8 +424,8 @@ class DfsRunner {
     for (const Frame* f = parent;; f = f->up) {
       find_.middle.push_back(static_cast<u32>(tag & 0xFFFF));
       const size_t idx = static_cast<size_t>(tag >> 16);
-      if (!f) {
-        find_.root_index = idx;
+      if (!f) {  // index into the shard's roots -> index into L_IBFS
+        find_.root_index = root_start_ + idx * root_stride_;
         break;
       }
       tag = dev::read_tag(c_, *f->list, idx);
@@ -434,6 +441,7 @@ class DfsRunner {
   bool tracking_;
   std::vector<std::array<u64, 5>>* log_;
   u64 bound_ = 0;
+  size_t root_start_ = 0, root_stride_ = 1;
   DfsFind find_;
   std::set<u64> dumped_;
 };
