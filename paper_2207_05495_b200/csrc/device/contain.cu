@@ -768,8 +768,26 @@ std::vector<uint8_t> superset_keep(Context& c, const PermIndex& p, const DList& 
 
 // Minimal antichain: drop every set with a proper subset in the list.
 // Rarest-state-first order prunes best here (queries are the keys themselves).
+size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper) {
+  if (b.empty() || A.empty()) return 0;
+  if (brute_fits(A.size(), b.size())) {
+    const size_t before = b.size();
+    auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+    brute_keep_flags(c, A, b, /*super=*/false, proper, keep);
+    return before - compact_flags(c, b, keep, nullptr);
+  }
+  const PermIndex p = build_perm_index(c, A, StateOrder::FreqDesc);
+  return remove_supersets(c, p, b, proper);
+}
+
 size_t self_reduce_minimal(Context& c, DList& l) {
   if (l.size() <= 1) return 0;
+  if (brute_fits(l.size(), l.size())) {  // small list: one all-pairs launch
+    const size_t before = l.size();
+    auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
+    brute_keep_flags(c, l, l, /*super=*/false, /*proper=*/true, keep);
+    return before - compact_flags(c, l, keep, nullptr);
+  }
   const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
   // The queries are the keys themselves: query with the index's own sorted,
   // relabelled rows (best locality), then map the flags back to l's order.

@@ -213,6 +213,20 @@ size_t self_reduce_maximal(Context& c, DList& l);
 // Self-reduction to the minimal antichain (subset_algebra.hpp:179-197).
 size_t self_reduce_minimal(Context& c, DList& l);
 
+// ---- all-pairs containment for small lists (brute.cu): one launch, no index.
+// The list paths above switch to it when |A|·|B| <= kBrutePairs.
+constexpr double kBrutePairs = 16.0 * 1024 * 1024;
+bool brute_fits(size_t na, size_t nb);
+// keep[j] = 1 iff no a in A relates to B[j]: super=false: a ⊆ B[j] (proper: ⊊);
+// super=true: B[j] ⊆ a (proper: ⊊).  keep is a device array of |B| bytes.
+void brute_keep_flags(Context& c, const DList& A, const DList& B, bool super, bool proper,
+                      uint8_t* keep);
+// Is some a ⊆ some b?  Witness indices are positions in A and B.
+bool brute_exists_subset(Context& c, const DList& A, const DList& B, Witness* w);
+// remove_supersets against a plain list A: all-pairs when small, else a
+// FreqDesc index over A.  Returns #removed.
+size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper);
+
 // ---- list surgery
 void keep_card_at_most(Context& c, DList& l, u32 max_card);
 void keep_card_at_least(Context& c, DList& l, u32 min_card);  // plain card of complements
@@ -224,6 +238,11 @@ DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool
 void merge_sorted(Context& c, DList& h, const DList& add);
 u64 read_tag(Context& c, const DList& l, size_t i);
 std::vector<u64> read_tags(Context& c, const DList& l);
+
+// ---- one beam level in one launch when it fits a CTA's shared memory
+// (beam.cu): sort (card desc, lex, index), drop duplicates, keep the first
+// `beam`; *top_card = the first survivor's card.  false: too large, untouched.
+bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card);
 
 // ---- static trie shape (static_trie.hpp:85-151) for exact ledger accounting
 u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);

@@ -179,6 +179,10 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
   const u64 ny = Y.size(), nx = X.size();
   cudaStream_t s = as_stream(c.stream());
   if (!ny) return;
+  if (brute_fits(nx, ny)) {  // small lists: one all-pairs launch
+    brute_keep_flags(c, X, Y, /*super=*/true, proper, keep);
+    return;
+  }
   SW_CUDA(cudaMemsetAsync(keep, 1, ny, s));
   if (!nx) return;
   const u32 n = c.n();

@@ -199,8 +199,7 @@ void GpuBibfs::bfs_step(bool with_history) {
   double r_hist = 0.0;
   if (with_history) {
     const size_t before = next.size();
-    const dev::PermIndex hix = dev::build_perm_index(ctx_, *hbfs_, dev::StateOrder::FreqDesc);
-    const size_t removed = dev::remove_supersets(ctx_, hix, next, /*proper=*/false);
+    const size_t removed = dev::remove_supersets_of(ctx_, *hbfs_, next, /*proper=*/false);
     r_hist = ratio(removed, before);
   }
   shrink_charge(next.size());
@@ -284,11 +283,19 @@ void GpuBibfs::perform(StepKind kind) {
 }
 
 // Meet: is some X in L_BFS a subset of some Y in L_IBFS?
-bool GpuBibfs::meet() { return dev::exists_subset(ctx_, bfs_index(), *libfs_, nullptr); }
+// Small lists: one all-pairs launch instead of building the index.
+bool GpuBibfs::meet() {
+  if (dev::brute_fits(lbfs_->size(), libfs_->size()))
+    return dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, nullptr);
+  return dev::exists_subset(ctx_, bfs_index(), *libfs_, nullptr);
+}
 
 bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
   dev::Witness w;
-  if (!dev::exists_subset(ctx_, bfs_index(), *libfs_, &w)) return false;
+  const bool met = dev::brute_fits(lbfs_->size(), libfs_->size())
+                       ? dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, &w)
+                       : dev::exists_subset(ctx_, bfs_index(), *libfs_, &w);
+  if (!met) return false;
   *bfs_index_out = w.a_index;
   *ibfs_tag = dev::read_tag(ctx_, *libfs_, w.b_index);
   return true;
