@@ -112,8 +112,7 @@ bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card) {
   DList out(&c, std::min(m, beam), next.tagged());
   u32* res = static_cast<u32*>(c.scratch(7, 64));
   SW_DISPATCH_W(c.W(), {
-    SW_CUDA(cudaFuncSetAttribute(beam_level_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kBeamSmem)));
+    smem_opt_in(reinterpret_cast<const void*>(beam_level_kernel<W>), static_cast<int>(kBeamSmem));
     beam_level_kernel<W><<<1, kBeamThreads, smem, s>>>(
         next.words, next.cards, next.tagged() ? next.tags : nullptr, static_cast<u32>(m),
         static_cast<u32>(m2), static_cast<u32>(std::min<size_t>(beam, 0xFFFFFFFFu)), out.words,

@@ -25,12 +25,7 @@ int device_count() {
   return n;
 }
 
-Context::Context(const Automaton& aut, int device)
-    : n_(aut.state_count()), k_(aut.alphabet_size()), W_(words_for(aut.state_count())) {
-  if (W_ > static_cast<u32>(kMaxW))
-    throw std::invalid_argument("n > 1024 states is not supported by the device kernels");
-  if (static_cast<u64>(n_) * k_ > 24576)
-    throw std::invalid_argument("n*k > 24576 transitions is not supported by the device kernels");
+Context::Context(const Automaton& aut, int device) {
   int ndev = device_count();
   if (ndev == 0) throw DeviceError("no CUDA device available (the B200 data plane has no CPU fallback)");
   if (device < 0) SW_CUDA(cudaGetDevice(&device));
@@ -44,6 +39,27 @@ Context::Context(const Automaton& aut, int device)
   SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
   u64 thresh = ~u64{0};
   SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  bind(aut);
+}
+
+// (Re)bind to an automaton: upload its tables, reset the counters.  The
+// stream and scratch buffers stay, so a worker thread reuses one context
+// for a whole batch of solves (experiment.cpp).
+void Context::bind(const Automaton& aut) {
+  const u32 n = aut.state_count(), k = aut.alphabet_size();
+  if (words_for(n) > static_cast<u32>(kMaxW))
+    throw std::invalid_argument("n > 1024 states is not supported by the device kernels");
+  if (static_cast<u64>(n) * k > 24576)
+    throw std::invalid_argument("n*k > 24576 transitions is not supported by the device kernels");
+  SW_CUDA(cudaSetDevice(device_));
+  if (d_img) free(const_cast<void*>(d_img));
+  if (d_poff) free(const_cast<void*>(d_poff));
+  if (d_psrc) free(const_cast<void*>(d_psrc));
+  n_ = n;
+  k_ = k;
+  W_ = words_for(n);
+  counters = Counters{};
+  timing = false;
 
   // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
   const InverseTransitions inv(aut);

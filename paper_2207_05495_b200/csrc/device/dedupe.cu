@@ -487,8 +487,7 @@ static size_t hash_dedupe_single(Context& c, DList& l) {
   SW_CUDA(cudaMemsetAsync(table, 0, static_cast<size_t>(nslots) * 4, s));
   SW_CUDA(cudaMemsetAsync(aux, 0, 16, s));
   const size_t smem = static_cast<size_t>(kDdThreads / 32) * single_warp_bytes<W>();
-  SW_CUDA(cudaFuncSetAttribute(dd_single_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  smem_opt_in(reinterpret_cast<const void*>(dd_single_kernel<W>), static_cast<int>(smem));
   DList out(&c, N, false);
   const unsigned grid = static_cast<unsigned>(
       std::min<u64>((ntiles + kDdThreads / 32 - 1) / (kDdThreads / 32), 148 * 8));
@@ -521,8 +520,7 @@ static size_t hash_dedupe_tiled(Context& c, DList& l) {
   SW_CUDA(cudaMemsetAsync(table, 0, static_cast<size_t>(nslots) * 4, s));
   SW_CUDA(cudaMemsetAsync(aux, 0, 16, s));
   const size_t smem = static_cast<size_t>(kDdThreads / 32) * (T * W * 8 + T * 12);
-  SW_CUDA(cudaFuncSetAttribute(dd_resolve_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  smem_opt_in(reinterpret_cast<const void*>(dd_resolve_kernel<W>), static_cast<int>(smem));
   const u64 per_pass = static_cast<u64>(kDdThreads) * rows_per_thread<W>();
   const unsigned grid_ins =
       static_cast<unsigned>(std::max<u64>(1, std::min<u64>((N + per_pass - 1) / per_pass, 148 * 8)));

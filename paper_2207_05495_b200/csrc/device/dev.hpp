@@ -110,6 +110,8 @@ class Context {
  public:
   Context(const Automaton& aut, int device = -1);
   ~Context();
+  // Re-target this context (stream, pool, scratch) to another automaton.
+  void bind(const Automaton& aut);
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
 
@@ -136,7 +138,7 @@ class Context {
   void* scratch(int slot, size_t bytes);
 
  private:
-  u32 n_, k_, W_;
+  u32 n_ = 0, k_ = 0, W_ = 0;
   int device_ = 0;
   void* stream_ = nullptr;
   struct Scratch { void* p = nullptr; size_t bytes = 0; };

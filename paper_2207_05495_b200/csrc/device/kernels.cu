@@ -259,9 +259,7 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
                                   : expand_sliced_kernel<W, false, true>)
                        : (inverse ? expand_sliced_kernel<W, true, false>
                                   : expand_sliced_kernel<W, false, false>);
-    if (shmem > 48 * 1024)
-      SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(shmem)));
+    if (shmem > 48 * 1024) smem_opt_in(reinterpret_cast<const void*>(kern), static_cast<int>(shmem));
     kern<<<grid, block, shmem, s>>>(src.words, lo, cnt, n, k,
                                     static_cast<const uint16_t*>(c.d_img),
                                     static_cast<const u32*>(c.d_poff),

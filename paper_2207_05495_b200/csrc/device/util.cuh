@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 #include "../common.hpp"
 
@@ -96,6 +99,30 @@ __device__ __forceinline__ void transpose64(u64 r0, u64 r1, int lane, u64& c0, u
   const u64 t1 = transpose32x2(r1, lane);  // [C^T_l | D^T_l]
   c0 = (t0 & 0xFFFFFFFF00000000ull) | (t1 >> 32);
   c1 = (t0 << 32) | (t1 & 0xFFFFFFFFull);
+}
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device,
+// once per (kernel, device): the attribute call takes driver locks, and many
+// solves run concurrently from one process's threads (config 2).
+inline void smem_opt_in(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device) at the max size
+  int dev = 0;
+  SW_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({kernel, dev})) return;
+  }
+  int max_optin = 0;
+  SW_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  (void)bytes;
+  cudaFuncAttributes fa{};
+  SW_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  // the largest dynamic size this kernel can use: later calls need no update
+  SW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               max_optin - static_cast<int>(fa.sharedSizeBytes)));
+  std::lock_guard<std::mutex> g(mu);
+  done.insert({kernel, dev});
 }
 
 inline int grid_for(size_t items, int block, int max_blocks = 148 * 16) {

@@ -530,6 +530,10 @@ void trace_line(std::ostream* trace, const GpuBibfs& eng, const SearchStats& s, 
 
 // --------------------------------------------------------------- solve
 SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
+  return solve_exact(aut, opt, nullptr);
+}
+
+SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Context* shared) {
   if (!is_synchronizing(aut)) throw NotSynchronizingError();
   SolveResult res;
   if (aut.state_count() == 1) {
@@ -537,7 +541,13 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
     if (opt.track_word) res.word = Word{};
     return res;
   }
-  dev::Context ctx(aut, opt.device);
+  std::unique_ptr<dev::Context> own;
+  if (shared) {
+    shared->bind(aut);
+  } else {
+    own = std::make_unique<dev::Context>(aut, opt.device);
+  }
+  dev::Context& ctx = shared ? *shared : *own;
   ctx.timing = opt.timing;
   using clock = std::chrono::steady_clock;
   const auto t0 = clock::now();

@@ -161,5 +161,8 @@ void trace_line(std::ostream* trace, const GpuBibfs& eng, const SearchStats& s, 
 }  // namespace detail
 
 SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt = {});
+// Same, on a caller-owned device context (re-bound to `aut`): a batch worker
+// keeps one context — stream, memory pool, scratch — across its solves.
+SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Context* ctx);
 
 }  // namespace synchro
