@@ -263,7 +263,7 @@ template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
     u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
-    u32* overflow_scans) {
+    u32* overflow_scans, unsigned long long* stats) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
@@ -431,6 +431,21 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       }
     }
 
+    if (stats) {  // analysis counters (SYNCHRO_PROGRESS): outcomes of this round's tasks
+      const bool internal = have && !is_leaf;
+      const bool minc_cut = internal && !brute && !longrun && c0 == kNone && L == 0;
+      const u32 v[8] = {
+          static_cast<u32>(__popc(__ballot_sync(FULL, have))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, have && is_leaf))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, hit))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, minc_cut))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, brute))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, internal && L != 0 && c0 == kNone))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, c0 != kNone))),
+          static_cast<u32>(__popc(__ballot_sync(FULL, c1 != kNone)))};
+      if (lane < 8) atomicAdd(stats + lane, static_cast<unsigned long long>(v[lane]));
+    }
+
     // ---- push children (LIFO; left on top)
     const u32 cdc = (cy << 16) | static_cast<u32>(dchild);
     const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
@@ -483,6 +498,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
       if (lane >= o) incl += v;
     }
     const u32 total = __shfl_sync(FULL, incl, 31);
+    if (stats && lane == 0) atomicAdd(stats + 8, static_cast<unsigned long long>(total));
     const u32 excl = incl - cnt;
     for (u32 base = 0; base < total; base += 32) {
       const u32 t = base + lane;
@@ -567,6 +583,11 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
+  unsigned long long* stats = nullptr;  // task-outcome counters, progress mode only
+  if (progress_enabled()) {
+    stats = static_cast<unsigned long long*>(c.scratch(7, 64 + 9 * 8)) + 8;  // after the Res words
+    SW_CUDA(cudaMemsetAsync(stats, 0, 9 * 8, s));
+  }
   uint4* spill = static_cast<uint4*>(
       c.scratch(10, static_cast<size_t>(grid) * kPoolWarps * kSpillCap * sizeof(uint4)));
   std::unique_ptr<StreamTimer> timer;
@@ -577,7 +598,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
-        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1);
+        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1, stats);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
@@ -591,6 +612,11 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
     if (progress_enabled()) {
       u32 overflow = 0;
       c.memcpy_d2h(&overflow, counter + 1, 4);
+      unsigned long long st[9];
+      c.memcpy_d2h(st, stats, sizeof(st));
+      SYNCHRO_PROGRESS("  contain-stats tasks=%llu leaf=%llu hit=%llu minc_cut=%llu brute=%llu "
+                       "prefix_cut=%llu push0=%llu push1=%llu pairs=%llu",
+                       st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8]);
       SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms overflow_scans=%u",
                        EXIST ? "exist" : "mark", PROPER ? "-proper" : "", p.count,
                        static_cast<unsigned long long>(Nb), ms, overflow);
