@@ -69,3 +69,14 @@ def test_exp_mark_and_powerset(oc, ref):
     for kat in kats[::7]:
         d = oc.random_automaton(kat["n"], kat["k"], kat["seed"])
         assert oc.power_set_oracle(kat["n"], kat["k"], d) == kat["oracle"]
+
+
+SLOW = json.load(open(os.path.join(GOLDEN, "slow_sync.json")))
+
+
+@pytest.mark.parametrize("case", SLOW, ids=[c["name"] for c in SLOW])
+def test_power_set_oracle_slow_sync(oc, case):
+    """Config 5: the extremal (slowly synchronizing) class, thresholds pinned by
+    the reference's power-set oracle in tests/golden/make_slow.py."""
+    d = np.asarray(case["delta"], np.uint32)
+    assert oc.power_set_oracle(case["n"], case["k"], d) == case["threshold"]
