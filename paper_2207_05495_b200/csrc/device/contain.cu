@@ -15,7 +15,8 @@
 //     y has state L (exactly the reference's "ones side recurses with B_1");
 //   * subtrees whose min cardinality exceeds |y| (|y|-1 for proper) are cut —
 //     the reference's per-pair card filter lifted to whole subtrees;
-//   * ranges of <= kPoolBrute keys are scanned (warp-cooperatively).
+//   * ranges of <= kScanKeys keys are scanned (warp-cooperatively) — unless the
+//     range's AND mask (states every key of it holds) has a state outside y.
 // The marked set {y : exists x in A, x ⊆ y (x ⊊ y)} does not depend on the
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
@@ -102,9 +103,15 @@ __global__ void karras_kernel(const u64* __restrict__ A, u32 N, Node* __restrict
 }
 
 // Bottom-up min cardinality: the second child to arrive at a node finishes it.
-__global__ void mincard_kernel(const u32* __restrict__ card, u32 N, Node* nodes,
-                               const u32* __restrict__ parent_int,
-                               const u32* __restrict__ parent_leaf, u32* arrivals) {
+// Nodes small enough to be scanned (<= small keys) also get the AND of their
+// keys: a query lacking one of those states cannot contain any of them, so the
+// scan is skipped (measured at n=300: 49% of meet/DFS scans, 61% of
+// self-reduction scans).
+template <int W>
+__global__ void mincard_kernel(const u32* __restrict__ card, const u64* __restrict__ keys, u32 N,
+                               Node* nodes, const u32* __restrict__ parent_int,
+                               const u32* __restrict__ parent_leaf, u32* arrivals, u64* andm,
+                               u32 small) {
   const u32 leaf = blockIdx.x * blockDim.x + threadIdx.x;
   if (leaf >= N) return;
   u32 p = parent_leaf[leaf];
@@ -117,10 +124,23 @@ __global__ void mincard_kernel(const u32* __restrict__ card, u32 N, Node* nodes,
     const u32 lm = (split == first) ? card[first] : vn[split].minc;
     const u32 rm = (split + 1 == last) ? card[last] : vn[split + 1].minc;
     vn[p].minc = static_cast<uint16_t>(lm < rm ? lm : rm);
+    if (last - first + 1 <= small) {
+      volatile u64* va = andm;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const u64 l = split == first ? keys[static_cast<u64>(first) * W + w]
+                                     : va[static_cast<u64>(split) * W + w];
+        const u64 r = split + 1 == last ? keys[static_cast<u64>(last) * W + w]
+                                        : va[static_cast<u64>(split + 1) * W + w];
+        va[static_cast<u64>(p) * W + w] = l & r;
+      }
+    }
     if (p == 0) return;
     p = parent_int[p];
   }
 }
+
+constexpr u32 kScanKeys = 16;  // nodes of <= this many keys are scanned, not descended
 
 ContainIndex build_index(Context& c, const DList& a) {
   ContainIndex ix;
@@ -135,7 +155,12 @@ ContainIndex build_index(Context& c, const DList& a) {
   u32* arr = static_cast<u32*>(c.alloc(static_cast<size_t>(N) * 4));
   SW_CUDA(cudaMemsetAsync(arr, 0, static_cast<size_t>(N) * 4, s));
   SW_DISPATCH_W(c.W(), { karras_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(a.words, N, nodes, pint, pleaf); });
-  mincard_kernel<<<(N + 255) / 256, 256, 0, s>>>(a.cards, N, nodes, pint, pleaf, arr);
+  ix.andmask = c.alloc(static_cast<size_t>(N - 1) * c.W() * 8);
+  SW_DISPATCH_W(c.W(), {
+    mincard_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(a.cards, a.words, N, nodes, pint, pleaf,
+                                                       arr, static_cast<u64*>(ix.andmask),
+                                                       kScanKeys);
+  });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 2;
   c.free(pint);
@@ -255,7 +280,7 @@ constexpr int kPoolThreads = kPoolWarps * 32;
 constexpr int kPoolCap = 256;
 constexpr int kSpill = kPoolCap / 2;
 constexpr int kSpillCap = 1024;  // tasks per warp in the global spill stack
-constexpr int kPoolBrute = 16;   // ranges of <= this many keys are scanned
+constexpr int kPoolBrute = kScanKeys;  // ranges of <= this many keys are scanned
 constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
 
@@ -263,7 +288,7 @@ template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
     u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
-    u32* overflow_scans, unsigned long long* stats) {
+    u32* overflow_scans, unsigned long long* stats, const u64* __restrict__ andm) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
@@ -409,6 +434,12 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
     // ---- round 2: whole query rows for brute ranges (their owner's row is
     // shuffled to the scanning lanes) and long common runs
     if (brute || longrun) load_row<W>(B, j, y, ycard);
+    if (brute) {  // every key of the range holds the node's AND states: all must be in y
+      u64 bad = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) bad |= __ldg(andm + static_cast<u64>(id) * W + w) & ~y[w];
+      if (bad) brute = false;
+    }
     if (longrun) {
       u32 kc;
       load_row<W>(A, nd.first, xf, kc);
@@ -598,7 +629,8 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
-        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1, stats);
+        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1, stats,
+        static_cast<const u64*>(p.tree.andmask));
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
@@ -614,7 +646,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
       c.memcpy_d2h(&overflow, counter + 1, 4);
       unsigned long long st[9];
       c.memcpy_d2h(st, stats, sizeof(st));
-      SYNCHRO_PROGRESS("  contain-stats tasks=%llu leaf=%llu hit=%llu minc_cut=%llu brute=%llu "
+      SYNCHRO_PROGRESS("  contain-stats tasks=%llu leaf=%llu hit=%llu minc_cut=%llu scans=%llu "
                        "prefix_cut=%llu push0=%llu push1=%llu pairs=%llu",
                        st[0], st[1], st[2], st[3], st[4], st[5], st[6], st[7], st[8]);
       SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms overflow_scans=%u",

@@ -306,9 +306,10 @@ std::vector<u64> read_tags(Context& c, const DList& l) {
 }
 
 ContainIndex::~ContainIndex() {
-  if (ctx && nodes) {
+  if (ctx) {
     try {
       ctx->free(nodes);
+      ctx->free(andmask);
     } catch (...) {
     }
   }
@@ -316,11 +317,16 @@ ContainIndex::~ContainIndex() {
 ContainIndex::ContainIndex(ContainIndex&& o) noexcept { *this = std::move(o); }
 ContainIndex& ContainIndex::operator=(ContainIndex&& o) noexcept {
   if (this != &o) {
-    if (ctx && nodes) ctx->free(nodes);
+    if (ctx) {
+      ctx->free(nodes);
+      ctx->free(andmask);
+    }
     nodes = o.nodes;
+    andmask = o.andmask;
     count = o.count;
     ctx = o.ctx;
     o.nodes = nullptr;
+    o.andmask = nullptr;
     o.count = 0;
   }
   return *this;

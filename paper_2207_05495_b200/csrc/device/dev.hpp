@@ -74,8 +74,9 @@ class ContainIndex {
   ~ContainIndex();
   ContainIndex(ContainIndex&&) noexcept;
   ContainIndex& operator=(ContainIndex&&) noexcept;
-  void* nodes = nullptr;  // device Node[N-1]
-  size_t count = 0;       // keys indexed
+  void* nodes = nullptr;    // device Node[N-1]
+  void* andmask = nullptr;  // analysis only (progress mode): per-node AND of the keys, W words
+  size_t count = 0;         // keys indexed
   Context* ctx = nullptr;
 };
 
