@@ -307,8 +307,15 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
   uint4* spill = spill_all + (static_cast<u64>(blockIdx.x) * kPoolWarps + wid) * kSpillCap;
   int sp = 0, gsp = 0;
   bool more = true;
+  // EXIST early exit: the flag is loaded each round but consumed the next, so
+  // its L2 round trip overlaps a round of work (a blocking check at the top of
+  // every round was 25% of the stall samples on the DFS queries).
+  int found_seen = 0;
   while (true) {
-    if (EXIST && *reinterpret_cast<volatile int*>(found)) break;
+    if (EXIST) {
+      if (found_seen) break;
+      found_seen = *reinterpret_cast<volatile int*>(found);
+    }
     if (sp < 32 && gsp > 0) {  // pull spilled tasks back first
       const int t = gsp < kSpill ? gsp : kSpill;
       for (int i = lane; i < t; i += 32) {
