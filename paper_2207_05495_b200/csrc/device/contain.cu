@@ -454,9 +454,9 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
 #pragma unroll
       for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
       if (!bad) {
-        u64 yl = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) yl = (w == (L >> 6)) ? y[w] : yl;
+        // query word L/64 straight from memory: a select over y[] here is
+        // turned into an indexed access that puts y and xf on the stack
+        const u64 yl = __ldg(B + static_cast<u64>(j) * Row<W>::P + (L >> 6));
         c0 = nd.split == nd.first ? (kLeafBit | nd.first) : nd.split;
         f0 = nd.first;
         if ((yl >> (63 - (L & 63))) & 1) {
@@ -481,7 +481,10 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
           static_cast<u32>(__popc(__ballot_sync(FULL, internal && L != 0 && c0 == kNone))),
           static_cast<u32>(__popc(__ballot_sync(FULL, c0 != kNone))),
           static_cast<u32>(__popc(__ballot_sync(FULL, c1 != kNone)))};
-      if (lane < 8) atomicAdd(stats + lane, static_cast<unsigned long long>(v[lane]));
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(stats + q, static_cast<unsigned long long>(v[q]));
+      }
     }
 
     // ---- push children (LIFO; left on top)
