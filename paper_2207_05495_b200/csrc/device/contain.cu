@@ -39,6 +39,24 @@ struct __align__(32) Node {
   u64 pad;
 };
 
+// One 256-bit load per node (LDG.E.ENL2.256 on sm_100a): a node visit is one
+// L1 wavefront instead of two 128-bit ones (the traversal is L1-bound).
+__device__ __forceinline__ Node load_node(const Node* p) {
+  unsigned long long w0, w1, w2, w3;
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+      : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+      : "l"(p));
+  Node nd;
+  nd.first = static_cast<u32>(w0);
+  nd.last = static_cast<u32>(w0 >> 32);
+  nd.split = static_cast<u32>(w1);
+  nd.lcp = static_cast<uint16_t>(w1 >> 32);
+  nd.minc = static_cast<uint16_t>(w1 >> 48);
+  nd.window = w2;
+  nd.pad = w3;
+  return nd;
+}
+
 // Bits [e-64, e) of an MSB-first bit string, right-aligned (bit e-1 at the
 // LSB; positions < 0 read as 0).  `at(w)` returns word w.
 template <class At>
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
         load_row<W>(B, j, y, ycard);
         load_row<W>(A, first, xf, kcard);
       } else {
-        nd = nodes[id];
+        nd = load_node(nodes + id);
         const u64* yr = B + static_cast<u64>(j) * Row<W>::P;
         ya = __ldg(yr + q0);
         yb = q0 + 1 < W ? __ldg(yr + q0 + 1) : 0;

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsynchro_b200.so")
+LIB_PATH = os.environ.get("SYNCHRO_B200_LIB") or os.path.join(HERE, "lib", "libsynchro_b200.so")
 CLI_PATH = os.path.join(HERE, "bin", "synchro")
 
 SW_OK = 0

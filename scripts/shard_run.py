@@ -5,7 +5,7 @@ MIN of their thresholds (distributed.py); run back to back on one B200, each
 shard's engine time is what its own GPU would spend.  Appends one JSON line per
 shard to the output file as it finishes (partial results survive a timeout).
 
-usage: shard_run.py SPEC UPPER_BOUND SHARDS OUT.jsonl [FIRST_SHARD]
+usage: shard_run.py SPEC UPPER_BOUND SHARDS OUT.jsonl [FIRST_SHARD [COUNT]]
 """
 import json
 import os
@@ -17,8 +17,9 @@ from paper_2207_05495_b200 import native as sw  # noqa: E402
 
 spec, ub, shards, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 first = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+count = int(sys.argv[6]) if len(sys.argv) > 6 else shards - first
 aut = sw.from_spec(spec)
-for s in range(first, shards):
+for s in range(first, min(shards, first + count)):
     t = time.perf_counter()
     r = sw.solve_exact(aut, upper_bound=ub, dfs_shard_index=s, dfs_shard_count=shards)
     row = {"spec": spec, "shard": s, "shards": shards, "threshold": r.threshold,
