@@ -303,7 +303,7 @@ constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
 
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kPoolThreads) contain_pool_kernel(
+__global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_kernel(
     const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
     u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
     u32* overflow_scans, unsigned long long* stats, const u64* __restrict__ andm) {
