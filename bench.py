@@ -256,12 +256,8 @@ def run_ours(args, world, rank, local):
         "warmup": max(3, args.warmup), "ms_per_step": dev_s_max * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (SplitMix64 random automaton, automaton.hpp:159-164)",
-        "config": {"workload": f"{args.workload} exact solve (engine; heuristic bound R={R} "
-                               "precomputed, bit-identical to the reference's)",
-                   "n": aut.n, "k": aut.k, "threshold": results[0].threshold,
-                   "expansions_per_solve": expansions,
-                   "l2": "flushed between timed steps (512 MiB write; device time excludes it)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": arm_config(args.workload, aut.n, aut.k, R, world, results[0].threshold,
+                             expansions),
         "time_to_threshold_s": statistics.median(x[0] for x in e2e),
         "engine_time_s": dev_s_max / args.steps,
         "e2e": {"value": e2e_units / e2e_s, "unit": UNIT,
@@ -306,6 +302,22 @@ def run_ours(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def arm_config(workload, n, k, R, world, threshold=None, expansions=None):
+    """The `config` both arms print (the driver compares the arms on it)."""
+    if threshold is None or expansions is None:  # bit-identical across implementations
+        gold = os.path.join(ROOT, "tests", "golden", "solve_" + workload.replace("random:", "random_")
+                            .replace(",", "_") + ".json")
+        if os.path.exists(gold):
+            g = json.load(open(gold))
+            threshold = g["threshold"]
+            expansions = g["expansions_phase1"] + g["expansions_dfs"]
+    return {"workload": f"{workload} exact solve (engine; heuristic bound R={R} precomputed, "
+                        "bit-identical to the reference's)",
+            "n": n, "k": k, "threshold": threshold, "expansions_per_solve": expansions,
+            "l2": "flushed between timed steps (512 MiB write; device time excludes it)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -332,8 +344,7 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (SplitMix64 random automaton)",
-        "config": {"workload": f"{args.workload} exact solve (engine; upper_bound={ub})",
-                   "n": n, "k": k},
+        "config": arm_config(args.workload, n, k, ub, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
                          "sample": f"reference engine on {args.workload}, first {its} iterations "
                                    f"per step ({per_step:.0f} s budget); single-threaded by "

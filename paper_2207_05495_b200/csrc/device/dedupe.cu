@@ -544,7 +544,9 @@ static size_t hash_dedupe_tiled(Context& c, DList& l) {
 size_t hash_dedupe(Context& c, DList& l) {
   const u64 N = l.size();
   if (N <= 1) return 0;
-  if (N >= kIdxMask) return hash_dedupe_wide(c, l);  // index does not fit 25 bits
+  // index does not fit 25 bits (SYNCHRO_DEDUPE_WIDE=1 forces this path: tests)
+  const char* wide = std::getenv("SYNCHRO_DEDUPE_WIDE");
+  if (N >= kIdxMask || (wide && *wide == '1')) return hash_dedupe_wide(c, l);
   size_t r = 0;
   if (l.tagged()) {  // tags differ between equal rows: the minimum index must win
     SW_DISPATCH_W(c.W(), { r = hash_dedupe_tiled<W>(c, l); });

@@ -104,6 +104,21 @@ def test_hash_dedupe_long_probe_chains(gpu, monkeypatch, tagged):
         assert _as_set(n, gw, gc) == _as_set(n, kw, gpu.cards_of(n, kw))
 
 
+@pytest.mark.parametrize("n", [20, 300, 570])
+def test_hash_dedupe_wide_table_path(gpu, monkeypatch, n):
+    """The 64-bit-entry table used for lists of >= 2^25 rows (forced here):
+    first occurrences survive, in their original order."""
+    monkeypatch.setenv("SYNCHRO_DEDUPE_WIDE", "1")
+    base = random_list(n, 3000, 0.1, 17).reshape(-1, W(n))
+    pick = np.random.default_rng(n).integers(0, base.shape[0], size=5000)
+    words = base[pick].reshape(-1)
+    tags = np.arange(5000, dtype=np.uint64) * 3
+    keep = _first_occurrence(n, words)
+    gw, _, gt = gpu.list_hash_dedupe(n, words, tags)
+    assert np.array_equal(gw.reshape(-1, W(n)), words.reshape(-1, W(n))[keep])
+    assert np.array_equal(gt, tags[keep])
+
+
 def test_hash_dedupe_empty(gpu):
     gw, gc, _ = gpu.list_hash_dedupe(100, np.zeros(0, np.uint64))
     assert gw.size == 0 and gc.size == 0
