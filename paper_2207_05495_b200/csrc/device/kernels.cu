@@ -100,8 +100,8 @@ constexpr size_t kStageSmemLimit = 200 * 1024;
 // Shared memory of the sliced kernel: per warp 64W input slices + 64W output
 // slices, and (STAGED) a 64·k·W-word child block + 64·k cards; then the table.
 template <int W>
-static size_t sliced_smem(u32 k, u32 n, bool staged) {
-  size_t per_warp = 2 * 64 * W * sizeof(u64);
+static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
+  size_t per_warp = (inverse ? 1 : 2) * 64 * W * sizeof(u64);  // preimage: no output slices
   if (staged) per_warp += static_cast<size_t>(64) * k * (W * sizeof(u64) + sizeof(u32));
   return kSliceWarps * per_warp + ((static_cast<size_t>(k) * n * 2 + 15) & ~size_t{15});
 }
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
   // [warps][64W] input slices, [warps][64W] output slices (image),
   // (STAGED) [warps][64kW] child block, [warps][64k] cards; table u16[k][n]
   u64* s_slices = reinterpret_cast<u64*>(smem);
-  unsigned char* p = smem + 2 * kSliceWarps * 64 * W * sizeof(u64);
+  unsigned char* p = smem + (INV ? 1 : 2) * kSliceWarps * 64 * W * sizeof(u64);
   u64* stage = nullptr;
   u32* scard = nullptr;
   if (STAGED) {
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
   for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
   __syncthreads();
   u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
-  u64* so = s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
+  u64* so = INV ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
   const u64 batches = (count + 63) / 64;
   for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
@@ -253,8 +253,8 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
   const u64 batches = (cnt + 63) / 64;
   const int grid = static_cast<int>(std::min<u64>((batches + kSliceWarps - 1) / kSliceWarps, 148 * 16));
   SW_DISPATCH_W(c.W(), {
-    const bool staged = sliced_smem<W>(k, n, true) <= kStageSmemLimit;
-    const size_t shmem = sliced_smem<W>(k, n, staged);
+    const bool staged = sliced_smem<W>(k, n, true, inverse) <= kStageSmemLimit;
+    const size_t shmem = sliced_smem<W>(k, n, staged, inverse);
     auto kern = staged ? (inverse ? expand_sliced_kernel<W, true, true>
                                   : expand_sliced_kernel<W, false, true>)
                        : (inverse ? expand_sliced_kernel<W, true, false>
