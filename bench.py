@@ -356,11 +356,12 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
+    if args.impl == "reference":  # CPU arm: rank 0 alone works, no process group needed
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")),
+                      int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = dist_setup(args.gpus)
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-    else:
-        run_ours(args, world, rank, local)
+    run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
