@@ -248,6 +248,14 @@ def run_ours(args, world, rank, local):
     dd_ms, dd_unique = sw.bench_dedupe(aut.n, mb_count, mb_density, seed=1, dup_fraction=0.1, iters=3)
     ls_ms, _ = sw.bench_dedupe(aut.n, mb_count, mb_density, seed=1, dup_fraction=0.1, iters=2,
                                lex_sort=True)
+    # Containment as work rather than bytes: one untimed solve with
+    # the traversal counters on; node visits + range-scan pair tests per second of
+    # the timed traversal, against the INT32 logic ceiling.
+    cs = sw.solve_exact(aut, upper_bound=R, device=local, contain_stats=True)
+    cont_ms_solve = cont_ms / len(results)
+    logic_rate = ((cs.contain_visits + cs.contain_pairs) / (cont_ms_solve / 1e3)
+                  if cont_ms_solve > 0 else None)
+    logic_ceiling = 148 * 128 * 1.965e9 / 10  # SMs x INT32 lanes x clock / ~10 LOP3 per W=5 test
     row = 8 * W + 4
     dd_bytes = mb_count * row + dd_unique * row  # read every candidate once + write survivors once
     dd_gbs = dd_bytes / (dd_ms / 1e3) / 1e9
@@ -274,7 +282,14 @@ def run_ours(args, world, rank, local):
                      "achieved": cont_gbs, "peak": roof_peak, "unit": "GB/s",
                      "frac": (cont_gbs / roof_peak) if cont_gbs else None,
                      "traffic": None, "share_of_step": cont_ms / engine_ms if engine_ms else None,
-                     "bytes_per_unit": f"{row} B per key/query row", "peak_source": peak_src},
+                     "bytes_per_unit": f"{row} B per key/query row", "peak_source": peak_src,
+                     "logic": {"unit": "node visits + pair tests /s", "achieved": logic_rate,
+                               "ceiling": logic_ceiling,
+                               "frac": logic_rate / logic_ceiling if logic_rate else None,
+                               "visits_per_solve": cs.contain_visits,
+                               "pair_tests_per_solve": cs.contain_pairs,
+                               "ceiling_source": "SURVEY §8(d): 148 SMs x 128 INT32 ops/clk x "
+                                                 "1.965 GHz / ~10 LOP3 per W=5 pair test"}},
         # North-star kernels at HBM scale (2^24 parents, n=300, density 0.077).
         "roofline_expand": {"bound": "hbm", "kernel": "expand_sliced_kernel",
                             "achieved": mb_exp_gbs, "achieved_preimage": mb_pre_gbs,

@@ -71,6 +71,7 @@ typedef struct sw_solve_options {
   int32_t timing;           /* 1: time expansion kernels with CUDA events */
   uint32_t dfs_shard_index; /* multi-GPU DFS partition: this process's share ... */
   uint32_t dfs_shard_count; /* ... of L_IBFS (threshold = MIN over shards); 1 = whole */
+  int32_t contain_stats;    /* 1: count containment-traversal node visits / pair tests */
 } sw_solve_options;
 
 /* SolveResult (bibfs_engine.hpp:50-59) + expansion counters and timings. */
@@ -96,6 +97,8 @@ typedef struct sw_solve_result {
   uint64_t d2h_bytes;       /* device->host bytes copied during the solve */
   double contain_kernel_ms; /* CUDA-event time of the containment traversal (timing=1) */
   uint64_t contain_bytes;   /* its algorithmic bytes (every key/query row read once) */
+  uint64_t contain_visits;  /* node visits of the traversal (contain_stats=1) */
+  uint64_t contain_pairs;   /* key-vs-query pair tests of its range scans (contain_stats=1) */
 } sw_solve_result;
 
 const char* sw_version(void);

@@ -91,6 +91,7 @@ SolveOptions to_options(const sw_solve_options* o) {
   s.tuning.dfs_reduce_cadence = o->reduce_cadence;
   s.device = o->device;
   s.timing = o->timing != 0;
+  s.contain_stats = o->contain_stats != 0;
   s.dfs_shard_count = std::max<uint32_t>(1, o->dfs_shard_count);
   s.dfs_shard_index = o->dfs_shard_index;
   if (s.dfs_shard_index >= s.dfs_shard_count) throw std::invalid_argument("dfs_shard_index >= dfs_shard_count");
@@ -206,6 +207,8 @@ SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
     out->kernel_launches = r.kernel_launches;
     out->contain_kernel_ms = r.contain_kernel_ms;
     out->contain_bytes = r.contain_bytes;
+    out->contain_visits = r.contain_visits;
+    out->contain_pairs = r.contain_pairs;
     out->engine_device_ms = r.engine_device_ms;
     out->h2d_bytes = r.h2d_bytes;
     out->d2h_bytes = r.d2h_bytes;

@@ -642,8 +642,8 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   const u64 want_blocks = (Nb + kPoolThreads - 1) / kPoolThreads;
   const unsigned grid = static_cast<unsigned>(
       std::max<u64>(1, std::min<u64>(want_blocks, static_cast<u64>(sms) * blocks_per_sm)));
-  unsigned long long* stats = nullptr;  // task-outcome counters, progress mode only
-  if (progress_enabled()) {
+  unsigned long long* stats = nullptr;  // task-outcome counters (progress mode / contain_stats)
+  if (progress_enabled() || c.contain_stats) {
     stats = static_cast<unsigned long long*>(c.scratch(7, 64 + 9 * 8)) + 8;  // after the Res words
     SW_CUDA(cudaMemsetAsync(stats, 0, 9 * 8, s));
   }
@@ -681,6 +681,12 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
                        EXIST ? "exist" : "mark", PROPER ? "-proper" : "", p.count,
                        static_cast<unsigned long long>(Nb), ms, overflow);
     }
+  }
+  if (c.contain_stats) {  // node visits (tasks) and range-scan pair tests of this launch
+    unsigned long long st[9];
+    c.memcpy_d2h(st, stats, sizeof(st));
+    c.counters.contain_visits += st[0];
+    c.counters.contain_pairs += st[8];
   }
 }
 

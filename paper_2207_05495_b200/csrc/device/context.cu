@@ -60,6 +60,7 @@ void Context::bind(const Automaton& aut) {
   W_ = words_for(n);
   counters = Counters{};
   timing = false;
+  contain_stats = false;
 
   // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
   const InverseTransitions inv(aut);

@@ -91,6 +91,8 @@ struct Counters {
   double contain_ms = 0;   // CUDA-event time of the traversal kernel (when timed)
   u64 contain_launches = 0;
   u64 contain_bytes = 0;   // algorithmic bytes of those launches
+  u64 contain_visits = 0;  // node visits (contain_stats)
+  u64 contain_pairs = 0;   // range-scan pair tests (contain_stats)
 };
 
 // CUDA-event pair on a context's stream (device-side span of a region).
@@ -133,6 +135,7 @@ class Context {
   const void* d_poff = nullptr;  // u16/u32[k*n+1] CSR offsets of the inverse
   const void* d_psrc = nullptr;  // u16[n*k] CSR sources
   bool timing = false;           // record CUDA-event time of expansion kernels
+  bool contain_stats = false;    // count traversal visits / pair tests (one readback per launch)
   Counters counters;
 
   // Scratch buffers reused across calls (grown on demand).

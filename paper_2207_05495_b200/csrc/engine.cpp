@@ -549,6 +549,7 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
   }
   dev::Context& ctx = shared ? *shared : *own;
   ctx.timing = opt.timing;
+  ctx.contain_stats = opt.contain_stats;
   using clock = std::chrono::steady_clock;
   const auto t0 = clock::now();
   std::optional<HeuristicResult> heur;
@@ -587,6 +588,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
     res.kernel_launches = ctx.counters.kernel_launches;
     res.contain_kernel_ms = ctx.counters.contain_ms;
     res.contain_bytes = ctx.counters.contain_bytes;
+    res.contain_visits = ctx.counters.contain_visits;
+    res.contain_pairs = ctx.counters.contain_pairs;
     return res;
   };
 

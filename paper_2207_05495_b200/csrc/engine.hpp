@@ -57,6 +57,7 @@ struct SolveOptions {
   // threshold of the whole search is the MIN over the shards.
   u32 dfs_shard_index = 0;
   u32 dfs_shard_count = 1;
+  bool contain_stats = false;  // count traversal node visits / pair tests (analysis)
 };
 
 struct SolveResult {
@@ -77,6 +78,8 @@ struct SolveResult {
   u64 kernel_launches = 0;
   double contain_kernel_ms = 0;  // CUDA-event time of the containment traversal (when timed)
   u64 contain_bytes = 0;         // its algorithmic bytes (keys + queries read once)
+  u64 contain_visits = 0;        // traversal node visits (contain_stats)
+  u64 contain_pairs = 0;         // range-scan pair tests (contain_stats)
   double engine_device_ms = 0;  // CUDA-event span of the engine on its stream
   u64 h2d_bytes = 0, d2h_bytes = 0;
   std::string phase;            // meet | dfs | bound | trivial

@@ -70,6 +70,7 @@ class SolveOptions(C.Structure):
         ("min_brute", C.c_uint32), ("min_leaf", C.c_uint32), ("dedupe_cadence", C.c_uint32),
         ("reduce_cadence", C.c_uint32), ("device", C.c_int32), ("timing", C.c_int32),
         ("dfs_shard_index", C.c_uint32), ("dfs_shard_count", C.c_uint32),
+        ("contain_stats", C.c_int32),
     ]
 
 
@@ -83,6 +84,7 @@ class SolveResultC(C.Structure):
         ("expand_kernel_ms", C.c_double), ("kernel_launches", C.c_uint64),
         ("phase", C.c_char * 16), ("engine_device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64), ("contain_kernel_ms", C.c_double), ("contain_bytes", C.c_uint64),
+        ("contain_visits", C.c_uint64), ("contain_pairs", C.c_uint64),
     ]
 
 
@@ -310,6 +312,8 @@ class SolveResult:
     contain_kernel_ms: float = 0.0
     contain_bytes: int = 0
     trace: Optional[List[str]] = field(default=None)
+    contain_visits: int = 0
+    contain_pairs: int = 0
 
     @property
     def expansions(self) -> int:
@@ -322,7 +326,7 @@ def default_options(**kw) -> SolveOptions:
     for key, v in kw.items():
         if key == "schedule" and isinstance(v, str):
             v = SCHEDULES[v]
-        if key in ("track_word", "timing"):
+        if key in ("track_word", "timing", "contain_stats"):
             v = int(bool(v))
         if v is None:
             continue
@@ -348,7 +352,8 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
                        bool(r.used_dfs), r.peak_memory, r.expansions_phase1, r.expansions_dfs,
                        r.heuristic_seconds, r.engine_seconds, r.expand_kernel_ms,
                        r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
-                       r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace)
+                       r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace,
+                       r.contain_visits, r.contain_pairs)
 
 
 ALGORITHMS = {"eppstein": 0, "beam": 1, "adaptive": 2}
