@@ -99,7 +99,162 @@ __global__ void __launch_bounds__(kBeamThreads) beam_level_kernel(
   }
 }
 
+// Whole beam search for small beams in ONE persistent CTA: every level's
+// preimages (child o = i·k + a: state p is in the child iff δ(p,a) is in
+// parent i), the (card desc, lex, index) bitonic sort, first-of-run dedupe,
+// truncation to `beam`, the per-level tags written out for the walk back, and
+// the stop test (top card == n) — no host round trip per level.
+template <int W>
+__global__ void __launch_bounds__(kBeamThreads) beam_full_kernel(
+    const uint16_t* __restrict__ g_img, u32 n, u32 k, u32 beam, u32 bc, u32 m2,
+    u32 max_levels, u64* __restrict__ level_tags, u32* __restrict__ result) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const u32 mmax = bc * k;
+  u64* cur = reinterpret_cast<u64*>(smem);                          // bc x W
+  u64* nxt = cur + static_cast<size_t>(bc) * W;                     // mmax x W
+  u32* ccard = reinterpret_cast<u32*>(nxt + static_cast<size_t>(mmax) * W);  // bc
+  u32* ncard = ccard + bc;                                          // mmax
+  u32* idx = ncard + mmax;                                          // m2
+  u32* keep = idx + m2;                                             // m2
+  uint16_t* img = reinterpret_cast<uint16_t*>(keep + m2);           // k x n
+  __shared__ u32 s_kept, s_done;
+  for (u32 i = threadIdx.x; i < k * n; i += kBeamThreads) img[i] = g_img[i];
+  for (u32 e = threadIdx.x; e < n * W; e += kBeamThreads) {  // level 0: the singletons
+    const u32 q = e / W, w = e % W;
+    cur[e] = (q >> 6) == w ? state_bit(q) : 0;
+  }
+  for (u32 q = threadIdx.x; q < n; q += kBeamThreads) ccard[q] = 1;
+  if (threadIdx.x == 0) s_done = 0;
+  __syncthreads();
+  u32 ncur = n, level = 0;
+  while (level < max_levels) {
+    ++level;
+    const u32 m = ncur * k;
+    for (u32 e = threadIdx.x; e < m * W; e += kBeamThreads) {  // preimages, one word each
+      const u32 o = e / W, w = e % W, i = o / k, a = o % k;
+      const u64* par = cur + static_cast<size_t>(i) * W;
+      u64 bits = 0;
+      const u32 p0 = 64 * w;
+      for (u32 b = 0; b < 64 && p0 + b < n; ++b) {
+        const u32 t = img[a * n + p0 + b];
+        bits |= ((par[t >> 6] >> (63 - (t & 63))) & 1ull) << (63 - b);
+      }
+      nxt[e] = bits;
+    }
+    __syncthreads();
+    for (u32 o = threadIdx.x; o < m; o += kBeamThreads) {
+      u32 c = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) c += __popcll(nxt[static_cast<size_t>(o) * W + w]);
+      ncard[o] = c;
+    }
+    u32 mp = 1;
+    while (mp < m) mp <<= 1;
+    for (u32 i = threadIdx.x; i < mp; i += kBeamThreads) idx[i] = i < m ? i : 0xFFFFFFFFu;
+    __syncthreads();
+    for (u32 size = 2; size <= mp; size <<= 1) {
+      for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+        for (u32 t = threadIdx.x; t < mp / 2; t += kBeamThreads) {
+          const u32 lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const u32 x = idx[lo], y = idx[hi];
+          bool y_first;
+          if (x == 0xFFFFFFFFu) y_first = y != 0xFFFFFFFFu;
+          else if (y == 0xFFFFFFFFu) y_first = false;
+          else y_first = beam_less<W>(nxt, ncard, y, x);
+          if (y_first == up) {
+            idx[lo] = y;
+            idx[hi] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (u32 p = threadIdx.x; p < m; p += kBeamThreads) {
+      bool first = p == 0;
+      if (!first) {
+        const u32 x = idx[p - 1], y = idx[p];
+        first = ncard[x] != ncard[y];
+#pragma unroll
+        for (int w = 0; w < W; ++w) first |= nxt[x * W + w] != nxt[y * W + w];
+      }
+      keep[p] = first ? 1u : 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 acc = 0;
+      for (u32 p = 0; p < m; ++p) {
+        const u32 v = keep[p];
+        keep[p] = v ? acc : 0xFFFFFFFFu;
+        acc += v;
+      }
+      s_kept = acc < beam ? acc : beam;
+      if (m && ncard[idx[0]] == n) s_done = 1;  // the first survivor is Q: a reset word
+    }
+    __syncthreads();
+    const u32 kept = s_kept;
+    for (u32 p = threadIdx.x; p < m; p += kBeamThreads) {  // survivors: tags out, rows to cur
+      const u32 r = keep[p];
+      if (r == 0xFFFFFFFFu || r >= beam) continue;
+      const u32 o = idx[p];
+      level_tags[static_cast<u64>(level - 1) * beam + r] = (static_cast<u64>(o / k) << 16) | (o % k);
+#pragma unroll
+      for (int w = 0; w < W; ++w) cur[static_cast<size_t>(r) * W + w] = nxt[static_cast<size_t>(o) * W + w];
+      ccard[r] = ncard[o];
+    }
+    __syncthreads();
+    ncur = kept;
+    if (s_done) break;
+  }
+  if (threadIdx.x == 0) {
+    result[0] = s_done ? level : 0;  // level of the reset word (0: none)
+    result[1] = level;               // levels run
+  }
+}
+
 }  // namespace
+
+BeamRun beam_full_small(Context& c, size_t beam, u64 level_cap, std::vector<u32>* word) {
+  const u32 n = c.n(), k = c.k(), W = c.W();
+  if (beam == 0 || beam > 4096) return BeamRun::NotApplicable;
+  const size_t bc = std::max<size_t>(n, beam), mmax = bc * k;
+  size_t m2 = 1;
+  while (m2 < mmax) m2 <<= 1;
+  const size_t smem = bc * W * 8 + mmax * W * 8 + bc * 4 + mmax * 4 + m2 * 8 +
+                      ((static_cast<size_t>(k) * n * 2 + 15) & ~size_t{15});
+  if (mmax > 8192 || smem > kBeamSmem) return BeamRun::NotApplicable;
+  const u64 max_levels = std::min<u64>(level_cap, 4096);
+  cudaStream_t s = as_stream(c.stream());
+  u64* tags = static_cast<u64*>(c.alloc(max_levels * beam * 8));
+  u32* res = static_cast<u32*>(c.scratch(7, 64));
+  SW_DISPATCH_W(c.W(), {
+    smem_opt_in(reinterpret_cast<const void*>(beam_full_kernel<W>), static_cast<int>(kBeamSmem));
+    beam_full_kernel<W><<<1, kBeamThreads, smem, s>>>(
+        static_cast<const uint16_t*>(c.d_img), n, k, static_cast<u32>(beam), static_cast<u32>(bc),
+        static_cast<u32>(m2), static_cast<u32>(max_levels), tags, res);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 1;
+  u32 h[2];
+  c.memcpy_d2h(h, res, 8);
+  BeamRun out;
+  if (h[0]) {  // walk the tags back from the reset set (index 0 of its level)
+    std::vector<u64> t(static_cast<size_t>(h[0]) * beam);
+    c.memcpy_d2h(t.data(), tags, t.size() * 8);
+    word->clear();
+    size_t i = 0;
+    for (u32 lvl = h[0]; lvl-- > 0;) {
+      const u64 tag = t[static_cast<size_t>(lvl) * beam + i];
+      word->push_back(static_cast<u32>(tag & 0xFFFF));
+      i = static_cast<size_t>(tag >> 16);
+    }
+    out = BeamRun::Found;
+  } else {
+    out = h[1] >= level_cap ? BeamRun::NotFound : BeamRun::NotApplicable;  // out of level room
+  }
+  c.free(tags);
+  return out;
+}
 
 bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card) {
   const size_t m = next.size();

@@ -249,6 +249,12 @@ std::vector<u64> read_tags(Context& c, const DList& l);
 // (beam.cu): sort (card desc, lex, index), drop duplicates, keep the first
 // `beam`; *top_card = the first survivor's card.  false: too large, untouched.
 bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card);
+// The whole beam search (from the singletons, at most level_cap levels) in one
+// single-CTA launch when the beam fits shared memory.  Found: *word = the reset
+// word (first letter first); NotFound: no word within level_cap;
+// NotApplicable: too large (or too many levels) — use the per-level path.
+enum class BeamRun { Found, NotFound, NotApplicable };
+BeamRun beam_full_small(Context& c, size_t beam, u64 level_cap, std::vector<u32>* word);
 
 // ---- static trie shape (static_trie.hpp:85-151) for exact ledger accounting
 u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);
