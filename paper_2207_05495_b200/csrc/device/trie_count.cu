@@ -130,21 +130,32 @@ __global__ void scatter_kernel(const u64* __restrict__ words, const u32* __restr
                                u32* __restrict__ cursor_zero, u32* __restrict__ cursor_one,
                                u32* __restrict__ idx_out, u32* __restrict__ seg_out) {
   const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  const u32 s = seg[i];
-  if (s == kInvalid) {
+  const int lane = threadIdx.x & 31;
+  const u32 s = i < N ? seg[i] : kInvalid;
+  if (i < N && s == kInvalid) {
     seg_out[i] = kInvalid;
     idx_out[i] = idx[i];
-    return;
   }
-  const u32 x = div[s];
-  const u32 e = idx[i];
-  const bool one = (words[static_cast<u64>(e) * W + (x >> 6)] >> (63 - (x & 63))) & 1;
-  u32 pos;
-  if (one)
-    pos = segs[s].lo + zcount[s] + atomicAdd(&cursor_one[s], 1u);
-  else
-    pos = segs[s].lo + atomicAdd(&cursor_zero[s], 1u);
+  const bool active = s != kInvalid;
+  u32 e = 0;
+  bool one = false;
+  if (active) {
+    const u32 x = div[s];
+    e = idx[i];
+    one = (words[static_cast<u64>(e) * W + (x >> 6)] >> (63 - (x & 63))) & 1;
+  }
+  // Warp-aggregated slot reservation: one atomic per (segment, side) group of
+  // the warp — near the root every element shares the same two cursors.
+  const u32 key = active ? (s << 1 | static_cast<u32>(one)) : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+  const int leader = __ffs(peers) - 1;
+  u32 base = 0;
+  if (active && lane == leader)
+    base = atomicAdd(one ? &cursor_one[s] : &cursor_zero[s], static_cast<u32>(__popc(peers)));
+  base = __shfl_sync(0xFFFFFFFFu, base, leader);
+  if (!active) return;
+  const u32 rank = __popc(peers & ((1u << lane) - 1));
+  const u32 pos = segs[s].lo + (one ? zcount[s] : 0) + base + rank;
   idx_out[pos] = e;
   seg_out[pos] = one ? child_one[s] : child_zero[s];
 }
