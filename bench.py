@@ -257,7 +257,8 @@ def run_ours(args, world, rank, local):
                   if cont_ms_solve > 0 else None)
     logic_ceiling = 148 * 128 * 1.965e9 / 10  # SMs x INT32 lanes x clock / ~10 LOP3 per W=5 test
     row = 8 * W + 4
-    dd_bytes = mb_count * row + dd_unique * row  # read every candidate once + write survivors once
+    dd_bytes = mb_count * row + dd_unique * row
+    traffic = dram_traffic(W, cont_bytes / len(results))  # read every candidate once + write survivors once
     dd_gbs = dd_bytes / (dd_ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -281,7 +282,8 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": "contain_pool_kernel (containment traversal)",
                      "achieved": cont_gbs, "peak": roof_peak, "unit": "GB/s",
                      "frac": (cont_gbs / roof_peak) if cont_gbs else None,
-                     "traffic": None, "share_of_step": cont_ms / engine_ms if engine_ms else None,
+                     "traffic": traffic["contain"], "traffic_note": traffic["contain_note"],
+                     "share_of_step": cont_ms / engine_ms if engine_ms else None,
                      "bytes_per_unit": f"{row} B per key/query row", "peak_source": peak_src,
                      "logic": {"unit": "node visits + pair tests /s", "achieved": logic_rate,
                                "ceiling": logic_ceiling,
@@ -297,6 +299,8 @@ def run_ours(args, world, rank, local):
                             "frac_preimage": mb_pre_gbs / roof_peak,
                             "bytes_per_unit": exp_bytes_per_child,
                             "ms_per_launch": mb_exp_ms, "children_per_launch": mb_count * aut.k,
+                            "traffic": traffic["expand"],
+                            "algorithmic_bytes_per_launch": mb_count * aut.k * exp_bytes_per_child,
                             "in_engine_achieved": achieved,
                             "in_engine_share_of_step": exp_ms / engine_ms if engine_ms else None},
         "roofline_dedupe": {"bound": "hbm", "kernel": "dd_single_kernel (one pass: hash claim in a "
@@ -304,6 +308,7 @@ def run_ours(args, world, rank, local):
                                                        "reservation; untagged frontier dedupe)",
                             "achieved": dd_gbs, "peak": roof_peak, "unit": "GB/s",
                             "frac": dd_gbs / roof_peak, "ms_per_call": dd_ms,
+                            "traffic": traffic["dedupe"], "algorithmic_bytes_per_launch": dd_bytes,
                             "sets": mb_count, "unique": dd_unique,
                             "lex_sort_dedupe_ms": ls_ms,
                             "lex_sort_dedupe_frac": dd_bytes / (ls_ms / 1e3) / 1e9 / roof_peak,
@@ -315,6 +320,30 @@ def run_ours(args, world, rank, local):
     line["clocks"] = clocks.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def dram_traffic(W, cont_bytes_per_solve):
+    """roofline.traffic: DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per
+    launch from the committed ncu captures of the same kernels on the same workload
+    (profiles/r01_dram_traffic.json, made by scripts/traffic_summary.py), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
+    out = {"contain": None, "contain_note": None, "expand": None, "dedupe": None}
+    if not os.path.exists(path):
+        return out
+    t = json.load(open(path))
+    cont = [v for k, v in t.items() if k.startswith(f"contain_pool_kernel<{W},")]
+    if cont:
+        launches = sum(v["launches"] for v in cont)
+        tb = sum(v["traffic_bytes_per_launch"] * v["launches"] for v in cont)
+        out["contain"] = tb / launches
+        out["contain_note"] = (f"ncu over one solve's {launches} traversal launches "
+                               f"({cont[0]['source']}); algorithmic bytes per launch "
+                               f"{cont_bytes_per_solve / launches:.3g}")
+    for key, name in (("expand", f"expand_sliced_kernel<{W}, 0, 1>"),
+                      ("dedupe", f"unnamed>::dd_single_kernel<{W}>")):
+        if name in t:
+            out[key] = t[name]["traffic_bytes_per_launch"]
+    return out
 
 
 def arm_config(workload, n, k, R, world, threshold=None, expansions=None):

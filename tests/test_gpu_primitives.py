@@ -184,3 +184,29 @@ def test_meet_check(gpu, ref, n, da, db, seed):
 def test_trie_node_count(gpu, ref, n, density, count, min_leaf):
     words = lex_sorted_unique(n, random_list(n, count, density, count + 1))
     assert gpu.trie_node_count(n, words, min_leaf) == ref.trie_node_count(n, words, min_leaf)[0]
+
+
+def _prefix_tie_list(n, count, seed):
+    """Rows whose leading words take only a few values, so the packed 64-bit
+    prefix key ties a lot and the order is decided by the refinement passes
+    over the later words (and, for equal rows, by the index tie-break)."""
+    rng = np.random.default_rng(seed)
+    words = random_list(n, count, 0.3, seed).reshape(-1, W(n))
+    for w in range(min(2, W(n) - 1)):
+        pool = random_list(n, 3, 0.5, seed + 100 + w).reshape(-1, W(n))[:, w]
+        words[:, w] = pool[rng.integers(0, 3, count)]
+    dup = rng.integers(0, count, count // 5)
+    words = np.concatenate([words, words[dup]])
+    return np.ascontiguousarray(words.reshape(-1))
+
+
+@pytest.mark.parametrize("n", [100, 300, 570])
+def test_sorts_with_prefix_ties(gpu, ref, n):
+    words = _prefix_tie_list(n, 4000, n)
+    tags = np.arange(words.size // W(n), dtype=np.uint64) * 3 + 1
+    gw, gc, gt = gpu.list_sort_card_desc_lex(n, words, tags)
+    rw, rc, rt = ref.sort_card_desc_lex(n, words, tags)
+    assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
+    gw, gc, gt = gpu.list_lex_sort_dedupe(n, words, tags)
+    rw, rc, rt, _ = ref.lex_sort_dedupe(n, words, tags)
+    assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
