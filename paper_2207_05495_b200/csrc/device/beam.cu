@@ -283,4 +283,118 @@ bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card) {
   return true;
 }
 
+// ---------------------------------------------------------------- large levels
+// A level's KEPT SET — the first `beam` distinct rows in (card desc, lex)
+// order — does not depend on the order the rows arrive in, and the next level
+// (the preimages of that set) does not depend on the kept rows' order either,
+// so the bound (the level at which Q is kept) is fixed by sets alone; only
+// the reconstructed word's letters can depend on order.  So instead of a full
+// (card desc, lex) sort of ~2·beam rows (≈ 8 radix passes per word): hash
+// dedupe (set semantics) → card histogram → the boundary class c* where the
+// running count from card n down reaches `beam` → every row with card > c*
+// is kept as is, and only the class card == c* is lex-sorted to take its
+// first beam − |card > c*| rows.
+namespace {
+__global__ void card_hist_kernel(const u32* __restrict__ cards, u64 N, u32 n, u32* __restrict__ hist) {
+  extern __shared__ u32 sh[];
+  for (u32 i = threadIdx.x; i <= n; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    atomicAdd(&sh[cards[i]], 1u);
+  __syncthreads();
+  for (u32 i = threadIdx.x; i <= n; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void card_class_kernel(const u32* __restrict__ cards, u64 N, u32 cs,
+                                  uint8_t* __restrict__ above, uint8_t* __restrict__ at) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 c = cards[i];
+    above[i] = c > cs;
+    at[i] = c == cs;
+  }
+}
+
+__global__ void find_card_kernel(const u32* __restrict__ cards, u64 N, u32 value,
+                                 unsigned long long* __restrict__ first) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (cards[i] == value) atomicMin(first, static_cast<unsigned long long>(i));
+}
+}  // namespace
+
+void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_index) {
+  const u32 n = c.n();
+  cudaStream_t s = as_stream(c.stream());
+  hash_dedupe(c, l);
+  const u64 N = l.size();
+  *top_card = 0;
+  *top_index = 0;
+  if (N == 0) return;
+  const size_t first_at = (static_cast<size_t>(n) + 2) & ~size_t{1};  // 8-B slot after the bins
+  auto* hist = static_cast<u32*>(c.scratch(7, first_at * 4 + 8));
+  SW_CUDA(cudaMemsetAsync(hist, 0, (static_cast<size_t>(n) + 1) * 4, s));
+  card_hist_kernel<<<grid_for(N, 256, 148 * 2), 256, (n + 1) * 4, s>>>(l.cards, N, n, hist);
+  SW_CHECK_LAUNCH();
+  std::vector<u32> h(n + 1);
+  c.memcpy_d2h(h.data(), hist, (static_cast<size_t>(n) + 1) * 4);
+  c.counters.kernel_launches += 1;
+  u32 top = 0;
+  for (u32 v = n + 1; v-- > 0;)
+    if (h[v]) {
+      top = v;
+      break;
+    }
+  if (N > beam) {
+    u64 cum = 0;
+    u32 cs = 0;
+    for (u32 v = n + 1; v-- > 0;) {
+      if (cum + h[v] >= beam) {
+        cs = v;
+        break;
+      }
+      cum += h[v];
+    }
+    const size_t need = beam - cum;  // rows taken from the boundary class
+    auto* above = static_cast<uint8_t*>(c.alloc(N));
+    auto* at = static_cast<uint8_t*>(c.scratch(5, N));
+    card_class_kernel<<<grid_for(N, 256), 256, 0, s>>>(l.cards, N, cs, above, at);
+    SW_CHECK_LAUNCH();
+    DList a = copy_list(c, l, true);
+    compact_flags(c, a, above, nullptr);
+    c.free(above);
+    compact_flags(c, l, at, nullptr);
+    if (l.size() > need) {
+      sort_lex(c, l);  // distinct rows: lex order decides
+      truncate(l, need);
+    }
+    DList out(&c, a.size() + l.size(), true);
+    const size_t W = c.W();
+    for (const DList* src : {&a, &l}) {
+      const size_t off = src == &a ? 0 : a.size(), cnt = src->size();
+      if (!cnt) continue;
+      SW_CUDA(cudaMemcpyAsync(out.words + off * W, src->words, cnt * W * 8, cudaMemcpyDeviceToDevice, s));
+      SW_CUDA(cudaMemcpyAsync(out.cards + off, src->cards, cnt * 4, cudaMemcpyDeviceToDevice, s));
+      SW_CUDA(cudaMemcpyAsync(out.tags + off, src->tags, cnt * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    out.set_size(a.size() + l.size());
+    l = std::move(out);
+    c.counters.kernel_launches += 1;
+  }
+  *top_card = top;
+  if (top == n) {  // Q was kept: its position starts the walk back
+    auto* first = reinterpret_cast<unsigned long long*>(hist + first_at);
+    const unsigned long long none = ~0ull;
+    c.memcpy_h2d(first, &none, 8);
+    find_card_kernel<<<grid_for(l.size(), 256), 256, 0, s>>>(l.cards, l.size(), n, first);
+    SW_CHECK_LAUNCH();
+    unsigned long long pos = 0;
+    c.memcpy_d2h(&pos, first, 8);
+    *top_index = static_cast<size_t>(pos);
+    c.counters.kernel_launches += 1;
+  }
+}
+
 }  // namespace synchro::dev

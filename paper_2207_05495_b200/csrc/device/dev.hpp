@@ -249,6 +249,10 @@ std::vector<u64> read_tags(Context& c, const DList& l);
 // (beam.cu): sort (card desc, lex, index), drop duplicates, keep the first
 // `beam`; *top_card = the first survivor's card.  false: too large, untouched.
 bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card);
+// Any-size beam level with the same KEPT SET as sort (card desc, lex) + dedupe +
+// truncate(beam), in unspecified order (beam.cu): *top_card = max kept card,
+// *top_index = the position of Q in `next` when *top_card == n.
+void beam_select(Context& c, DList& next, size_t beam, u32* top_card, size_t* top_index);
 // The whole beam search (from the singletons, at most level_cap levels) in one
 // single-CTA launch when the beam fits shared memory.  Found: *word = the reset
 // word (first letter first); NotFound: no word within level_cap;
