@@ -219,6 +219,8 @@ def run_ours(args, world, rank, local):
 
     # e2e: public call, host transition table in, threshold + word out, heuristic included.
     e2e = []
+    for _ in range(2):  # untimed warm-up of the public path (first use of the heuristic kernels)
+        sw.solve_exact(aut, device=local, track_word=True)
     for _ in range(max(1, min(args.steps, 3))):
         flush_l2(local)
         t = time.perf_counter()
