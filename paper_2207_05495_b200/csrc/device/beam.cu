@@ -366,9 +366,12 @@ void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_i
     compact_flags(c, a, above, nullptr);
     c.free(above);
     compact_flags(c, l, at, nullptr);
-    if (l.size() > need) {
-      sort_lex(c, l);  // distinct rows: lex order decides
-      truncate(l, need);
+    if (l.size() > need) {  // one card class of distinct rows: lex order decides
+      u32 t = 0;
+      if (!beam_level_small(c, l, need, &t)) {  // single-CTA sort + truncate when it fits
+        sort_lex(c, l);
+        truncate(l, need);
+      }
     }
     DList out(&c, a.size() + l.size(), true);
     const size_t W = c.W();
