@@ -175,6 +175,20 @@ int sw_list_hash_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, uint64_t* 
                         size_t count, size_t* out_count);
 int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards, size_t count,
                                 size_t* out_count);
+/* Multi-GPU frontier exchange building blocks (no reference
+ * counterpart — the reference is single-threaded per solve).  DEVICE pointers
+ * on the current device (e.g. torch CUDA tensors); synchronous.
+ * sw_dev_owner_partition regroups `count` rows owner-major by
+ * owner = h(row) mod nranks (h restated in tests/test_distributed_cpu.py),
+ * writing out_words/out_cards and counts[r] (host) = rows owned by rank r;
+ * order inside an owner's segment is unspecified.  nranks in [1, 1024].
+ * sw_dev_hash_dedupe: set-semantics dedupe of a device-resident list, compacted
+ * in place; *kept = survivors (distributed.py owner_exchange_dedupe). */
+int sw_dev_owner_partition(uint32_t n, const uint64_t* d_words, const uint32_t* d_cards,
+                           uint64_t count, uint32_t nranks, uint64_t* d_out_words,
+                           uint32_t* d_out_cards, uint64_t* counts);
+int sw_dev_hash_dedupe(uint32_t n, uint64_t* d_words, uint32_t* d_cards, uint64_t count,
+                       uint64_t* kept);
 /* keep[j] = 1 iff b[j] is NOT marked.  mode 0: supersets (incl. equal),
  * 1: proper supersets, 2: subsets.  a must be lex-sorted unique for modes 0/1
  * (require_sorted_unique, subset_algebra.hpp:127-130) else SW_ERR_PARSE. */

@@ -384,6 +384,54 @@ SW_EXPORT int sw_list_hash_dedupe(uint32_t n, uint64_t* words, uint32_t* cards, 
                  [](dev::Context& c, dev::DList& l) { dev::hash_dedupe(c, l); });
 }
 
+namespace {
+// Device-resident list in/out (the exchange runs on the caller's tensors).
+dev::DList device_in(dev::Context& c, const uint64_t* d_words, const uint32_t* d_cards, uint64_t count) {
+  dev::DList l(&c, count, false);
+  const size_t W = c.W();
+  if (count) {
+    c.memcpy_d2d(l.words, d_words, count * W * 8);
+    c.memcpy_d2d(l.cards, d_cards, count * 4);
+  }
+  l.set_size(count);
+  return l;
+}
+void device_out(dev::Context& c, const dev::DList& l, uint64_t* d_words, uint32_t* d_cards) {
+  if (l.size()) {
+    c.memcpy_d2d(d_words, l.words, l.size() * c.W() * 8);
+    c.memcpy_d2d(d_cards, l.cards, l.size() * 4);
+  }
+  c.sync();
+}
+}  // namespace
+
+SW_EXPORT int sw_dev_owner_partition(uint32_t n, const uint64_t* d_words, const uint32_t* d_cards,
+                                     uint64_t count, uint32_t nranks, uint64_t* d_out_words,
+                                     uint32_t* d_out_cards, uint64_t* counts) {
+  if (nranks == 0 || nranks > 1024 || !counts) {
+    g_last_error = "owner_partition: nranks must be in [1, 1024]";
+    return SW_ERR_PARSE;
+  }
+  return guarded([&] {
+    dev::Context c(identity_aut(n));  // the caller's current device
+    dev::DList l = device_in(c, d_words, d_cards, count);
+    const std::vector<u64> per = dev::owner_partition(c, l, nranks);
+    device_out(c, l, d_out_words, d_out_cards);
+    for (uint32_t r = 0; r < nranks; ++r) counts[r] = r < per.size() ? per[r] : 0;
+  });
+}
+
+SW_EXPORT int sw_dev_hash_dedupe(uint32_t n, uint64_t* d_words, uint32_t* d_cards, uint64_t count,
+                                 uint64_t* kept) {
+  return guarded([&] {
+    dev::Context c(identity_aut(n));  // the caller's current device
+    dev::DList l = device_in(c, d_words, d_cards, count);
+    dev::hash_dedupe(c, l);
+    device_out(c, l, d_words, d_cards);
+    if (kept) *kept = l.size();
+  });
+}
+
 SW_EXPORT int sw_list_self_reduce_minimal(uint32_t n, uint64_t* words, uint32_t* cards,
                                           size_t count, size_t* out_count) {
   if (!sorted_unique(words, count, words_for(n))) {

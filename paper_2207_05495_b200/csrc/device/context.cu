@@ -103,6 +103,10 @@ void Context::free(void* p) {
   if (p) SW_CUDA(cudaFreeAsync(p, as_stream(stream_)));
 }
 
+void Context::memcpy_d2d(void* dst, const void* src, size_t bytes) {
+  if (bytes) SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream_)));
+}
+
 void Context::sync() { SW_CUDA(cudaStreamSynchronize(as_stream(stream_))); }
 
 StreamTimer::StreamTimer(Context& c) : c_(c) {

@@ -129,6 +129,7 @@ class Context {
   void sync();
   void memcpy_d2h(void* dst, const void* src, size_t bytes);
   void memcpy_h2d(void* dst, const void* src, size_t bytes);
+  void memcpy_d2d(void* dst, const void* src, size_t bytes);  // stream-ordered
 
   // Transition tables in device memory (uploaded once).
   const void* d_img = nullptr;   // u16[k*n]  delta(q,a) at [a*n+q]
@@ -174,6 +175,9 @@ size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
 // Tagged lists keep the first occurrence's tag (minimum index, the
 // reference's survivor).  Returns #removed.
 size_t hash_dedupe(Context& c, DList& l);
+// Hash ownership (exchange.cu): regroups l owner-major by owner = h(row) mod
+// nranks (order inside an owner's segment unspecified); returns the rows per owner.
+std::vector<u64> owner_partition(Context& c, DList& l, u32 nranks);
 
 // ---- containment (subset_algebra.hpp:138-231, static_trie.hpp:51-55)
 // Radix tree over a lex-sorted unique list (internal building block).

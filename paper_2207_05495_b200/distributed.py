@@ -40,3 +40,53 @@ def solve_exact_sharded(aut, rank: int, world: int, solve: Optional[Callable] = 
     dist.all_gather_object(gathered, (int(res.threshold), res.word, rank), group=group)
     thr, word, _ = combine(gathered)
     return thr, word, res
+
+
+# ------------------------------------------------------------------ hash ownership
+def owner_hash(words, W: int, nranks: int):
+    """Owner rank of each row (numpy uint64 [N*W]) — the hash of exchange.cu,
+    restated for the CPU tests: h = 0x9E3779B97F4A7C15; per word w:
+    h = (h ^ w) * 0xff51afd7ed558ccd; h ^= h >> 32; owner = h mod nranks."""
+    import numpy as np
+    rows = np.asarray(words, np.uint64).reshape(-1, W)
+    h = np.full(rows.shape[0], 0x9E3779B97F4A7C15, np.uint64)
+    with np.errstate(over="ignore"):
+        for w in range(W):
+            h = (h ^ rows[:, w]) * np.uint64(0xFF51AFD7ED558CCD)
+            h ^= h >> np.uint64(32)
+    return (h % np.uint64(nranks)).astype(np.int64)
+
+
+def owner_exchange_dedupe(n: int, words, cards, group=None, partition=None, dedupe=None):
+    """Exact distributed dedupe of one generated level by hash ownership
+    (SURVEY §8(e)): every rank regroups its rows owner-major (device kernel,
+    sw_dev_owner_partition), ONE all-to-all (NCCL over NVLink on GPUs) carries
+    each row to its owner, and the owner dedupes what it received
+    (sw_dev_hash_dedupe).  Equal rows share an owner, so the union over ranks
+    of the returned lists is the deduplicated level, each value on exactly one
+    rank.  words: int64 view of the u64 rows [N*W], cards: int32 [N], on this
+    rank's device.  Returns (words, cards, bytes_sent) — bytes_sent counts the
+    rows this rank sent to other ranks (the NVLink payload).
+    `partition`/`dedupe` are injectable for the CPU (gloo) tests."""
+    import torch
+    import torch.distributed as dist
+    from . import native
+    W = native.W(n)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if partition is None:
+        partition = lambda w, c, k: native.dev_owner_partition(n, w, c, k)  # noqa: E731
+    if dedupe is None:
+        dedupe = lambda w, c: native.dev_hash_dedupe(n, w, c)  # noqa: E731
+    pw, pc, counts = partition(words, cards, world)
+    send = torch.tensor(counts, dtype=torch.int64, device=cards.device)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    rcounts = [int(x) for x in recv.tolist()]
+    rw = torch.empty(sum(rcounts) * W, dtype=words.dtype, device=words.device)
+    rc = torch.empty(sum(rcounts), dtype=cards.dtype, device=cards.device)
+    dist.all_to_all_single(rw, pw, [c * W for c in rcounts], [c * W for c in counts], group=group)
+    dist.all_to_all_single(rc, pc, rcounts, counts, group=group)
+    bytes_sent = sum(c for r, c in enumerate(counts) if r != rank) * (8 * W + 4)
+    ow, oc = dedupe(rw, rc)
+    return ow, oc, bytes_sent

@@ -33,7 +33,8 @@ EXPORTED_SYMBOLS = [
     "sw_list_expand", "sw_list_lex_sort_dedupe", "sw_list_sort_card_desc_lex",
     "sw_list_dedupe_sorted", "sw_list_hash_dedupe", "sw_list_self_reduce_minimal", "sw_list_mark",
     "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
-    "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe",
+    "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe", "sw_dev_owner_partition",
+    "sw_dev_hash_dedupe",
 ]
 
 
@@ -170,6 +171,10 @@ def load():
                                   C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     L.sw_bench_dedupe.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_int32,
                                   C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+    L.sw_dev_owner_partition.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                         C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+    L.sw_dev_hash_dedupe.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]
     _lib = L
     return L
 
@@ -491,6 +496,29 @@ def list_hash_dedupe(n: int, words: np.ndarray, tags: Optional[np.ndarray] = Non
     _check(load().sw_list_hash_dedupe(n, w, c, _tags_ptr(t), c.size, C.byref(out)))
     m = out.value
     return w[: m * W(n)], c[:m], (t[:m] if t is not None else None)
+
+
+def dev_owner_partition(n: int, words, cards, nranks: int):
+    """Device tensors (torch, current CUDA device): rows regrouped owner-major by
+    owner = h(row) mod nranks -> (words, cards, counts per owner)."""
+    import torch
+    words, cards = words.contiguous(), cards.contiguous()
+    count = cards.numel()
+    ow, oc = torch.empty_like(words), torch.empty_like(cards)
+    counts = (C.c_uint64 * nranks)()
+    _check(load().sw_dev_owner_partition(n, words.data_ptr(), cards.data_ptr(), count, nranks,
+                                         ow.data_ptr(), oc.data_ptr(), counts))
+    return ow, oc, [int(x) for x in counts]
+
+
+def dev_hash_dedupe(n: int, words, cards):
+    """Set-semantics dedupe of device tensors -> (words, cards) of the survivors."""
+    words, cards = words.contiguous().clone(), cards.contiguous().clone()
+    kept = C.c_uint64()
+    _check(load().sw_dev_hash_dedupe(n, words.data_ptr(), cards.data_ptr(), cards.numel(),
+                                     C.byref(kept)))
+    m = kept.value
+    return words.view(-1, W(n))[:m].reshape(-1), cards[:m]
 
 
 def list_self_reduce_minimal(n: int, words: np.ndarray) -> np.ndarray:

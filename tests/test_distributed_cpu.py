@@ -73,3 +73,82 @@ def test_two_rank_gloo_paths():
 def test_combine_prefers_min_then_lowest_rank():
     from paper_2207_05495_b200.distributed import combine
     assert combine([(5, "a", 0), (4, "b", 1), (4, "c", 2)]) == (4, "b", 1)
+
+
+EXCHANGE_WORKER = r"""
+import os, sys, json
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch
+import torch.distributed as dist
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=2)
+rank = dist.get_rank()
+from paper_2207_05495_b200 import distributed
+n, W = 130, 3
+rng = np.random.default_rng(5)
+base = rng.integers(0, 2**63, size=(400, W), dtype=np.int64)
+base[:, -1] &= ~((1 << 62) - 1)  # tail bits beyond n stay zero
+mine = base[rng.integers(0, 400, 700 + 50 * rank)]  # both ranks draw from one pool: duplicates across ranks
+
+def partition(w, c, k):  # test stand-in for the device kernel: same owner hash, grouped owner-major
+    rows = w.numpy().reshape(-1, W)
+    own = distributed.owner_hash(rows.view(np.uint64).reshape(-1), W, k)
+    order = np.argsort(own, kind="stable")
+    counts = np.bincount(own, minlength=k).tolist()
+    return (torch.from_numpy(rows[order].reshape(-1).copy()), torch.from_numpy(c.numpy()[order].copy()),
+            counts)
+
+def dedupe(w, c):
+    rows = w.numpy().reshape(-1, W)
+    _, first = np.unique(rows, axis=0, return_index=True)
+    return torch.from_numpy(rows[np.sort(first)].reshape(-1).copy()), c[np.sort(first)]
+
+w = torch.from_numpy(mine.reshape(-1).copy())
+c = torch.from_numpy(np.array([bin(int(x) & (2**64 - 1)).count("1") for x in mine.sum(axis=1)], np.int32))
+ow, oc, sent = distributed.owner_exchange_dedupe(n, w, c, partition=partition, dedupe=dedupe)
+out = {{"rank": rank, "rows": [list(map(int, r)) for r in ow.numpy().reshape(-1, W)], "sent": sent,
+       "mine": [list(map(int, r)) for r in mine]}}
+print(json.dumps(out))
+dist.destroy_process_group()
+"""
+
+
+def test_owner_exchange_dedupe_two_ranks():
+    """Hash-ownership exchange over a world_size-2 gloo group: every distinct row
+    ends on exactly one rank (its owner), duplicates across ranks collapse."""
+    import json
+    import socket
+
+    import numpy as np
+
+    from paper_2207_05495_b200.distributed import owner_hash
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    code = EXCHANGE_WORKER.format(root=ROOT, port=port)
+    procs = [subprocess.Popen([sys.executable, "-c", code, str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+    res = sorted((json.loads(o.strip().splitlines()[-1]) for o, _ in outs), key=lambda r: r["rank"])
+    every = {tuple(r) for x in res for r in x["mine"]}
+    got = [tuple(r) for x in res for r in x["rows"]]
+    assert len(got) == len(set(got)) and set(got) == every
+    for x in res:
+        rows = np.array(x["rows"], np.int64).view(np.uint64).reshape(-1)
+        assert (owner_hash(rows, 3, 2) == x["rank"]).all()
+        sent_rows = sum(1 for r in x["mine"]
+                        if owner_hash(np.array(r, np.int64).view(np.uint64), 3, 2)[0] != x["rank"])
+        assert x["sent"] == sent_rows * (8 * 3 + 4)
+
+
+def test_owner_hash_is_a_function_of_the_row():
+    import numpy as np
+
+    from paper_2207_05495_b200.distributed import owner_hash
+    rows = np.arange(40, dtype=np.uint64).reshape(20, 2)
+    a = owner_hash(rows.reshape(-1), 2, 8)
+    b = owner_hash(np.concatenate([rows, rows[::-1]]).reshape(-1), 2, 8)
+    assert (a == b[:20]).all() and (a[::-1] == b[20:]).all() and set(a.tolist()) <= set(range(8))

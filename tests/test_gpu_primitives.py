@@ -4,6 +4,8 @@ called through the C-ABI (include/synchro_b200.h) on seeded random lists.
 Bar: bit-exact — same words, same order, same cardinalities, same surviving
 tags (which duplicate survives, set_list.hpp:208-209).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -210,3 +212,66 @@ def test_sorts_with_prefix_ties(gpu, ref, n):
     gw, gc, gt = gpu.list_lex_sort_dedupe(n, words, tags)
     rw, rc, rt, _ = ref.lex_sort_dedupe(n, words, tags)
     assert np.array_equal(gw, rw) and np.array_equal(gc, rc) and np.array_equal(gt, rt)
+
+
+@pytest.mark.parametrize("n,nranks", [(300, 1), (300, 2), (300, 3), (570, 8), (100, 5)])
+def test_dev_owner_partition_matches_owner_hash(gpu, n, nranks):
+    """sw_dev_owner_partition (exchange.cu) groups rows owner-major by the owner
+    hash restated in distributed.owner_hash; rows keep their cards."""
+    import torch
+
+    from paper_2207_05495_b200.distributed import owner_hash
+    base = random_list(n, 3000, 0.08, n + nranks)
+    words = np.concatenate([base, base[: 500 * W(n)]])
+    cards = gpu.cards_of(n, words).astype(np.int32)
+    tw = torch.from_numpy(words.view(np.int64)).cuda()
+    tc = torch.from_numpy(cards).cuda()
+    ow, oc, counts = gpu.dev_owner_partition(n, tw, tc, nranks)
+    own = owner_hash(words, W(n), nranks)
+    assert counts == np.bincount(own, minlength=nranks).tolist()
+    ow = ow.cpu().numpy().view(np.uint64).reshape(-1, W(n))
+    oc = oc.cpu().numpy()
+    start = 0
+    for r, cnt in enumerate(counts):
+        seg = ow[start:start + cnt]
+        assert (owner_hash(seg.reshape(-1), W(n), nranks) == r).all()
+        start += cnt
+    assert sorted(map(tuple, ow.tolist())) == sorted(rows(n, words))
+    assert (oc == gpu.cards_of(n, ow.reshape(-1))).all()
+
+
+def test_dev_hash_dedupe_and_world1_nccl_exchange(gpu, tmp_path):
+    """Device-pointer dedupe, and owner_exchange_dedupe through a real NCCL
+    group of one rank (the all-to-all path the 8-GPU run takes)."""
+    import subprocess
+    import sys
+
+    import torch
+    n = 300
+    base = random_list(n, 4000, 0.08, 3)
+    words = np.concatenate([base, base[: 1500 * W(n)]])
+    cards = gpu.cards_of(n, words).astype(np.int32)
+    dw, dc = gpu.dev_hash_dedupe(n, torch.from_numpy(words.view(np.int64)).cuda(),
+                                 torch.from_numpy(cards).cuda())
+    got = dw.cpu().numpy().view(np.uint64)
+    assert sorted(rows(n, got)) == sorted(set(rows(n, words)))
+    np.save(tmp_path / "w.npy", words)
+    code = f"""
+import sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:{29500 + os.getpid() % 1000}", rank=0, world_size=1)
+torch.cuda.set_device(0)
+from paper_2207_05495_b200 import distributed, native
+w = np.load({str(tmp_path / "w.npy")!r})
+c = native.cards_of({n}, w).astype(np.int32)
+ow, oc, sent = distributed.owner_exchange_dedupe({n}, torch.from_numpy(w.view(np.int64)).cuda(),
+                                                 torch.from_numpy(c).cuda())
+np.save({str(tmp_path / "o.npy")!r}, ow.cpu().numpy().view(np.uint64))
+print("sent", sent)
+dist.destroy_process_group()
+"""
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]
+    out = np.load(tmp_path / "o.npy")
+    assert sorted(rows(n, out)) == sorted(set(rows(n, words)))
+    assert "sent 0" in p.stdout
