@@ -137,6 +137,50 @@ def sum_over_ranks(world, x: float) -> float:
     return float(t.item())
 
 
+# ------------------------------------------------------------ frontier exchange (N>1)
+def exchange_probe(n: int, world: int, rank: int, rows: int = 1 << 20, reps: int = 3):
+    """Hash-ownership exchange of one generated level (SURVEY §8(e),
+    distributed.owner_exchange_dedupe): every rank holds `rows` sets at the
+    frontier density (drawn from one shared pool, so duplicates span ranks),
+    regroups them by owner on the device, ONE NCCL all-to-all carries them to
+    their owners, the owners dedupe.  Reported: max-over-ranks device time and
+    the bytes that crossed NVLink (rows sent to other ranks x (8W+4))."""
+    import numpy as np
+    import torch
+    from paper_2207_05495_b200 import distributed, native as sw
+    W = sw.W(n)
+    pool_rng = np.random.default_rng(12345)
+    pool = pool_rng.integers(0, 2**63, size=(rows, W), dtype=np.int64).view(np.uint64)
+    for _ in range(3):  # density ~1/16 per bit
+        pool &= pool_rng.integers(0, 2**63, size=(rows, W), dtype=np.int64).view(np.uint64) << np.uint64(1)
+    if n % 64:
+        pool[:, -1] &= ~np.uint64(0) << np.uint64(64 - n % 64)
+    mine = pool[np.random.default_rng(rank + 1).integers(0, rows, rows)]
+    cards = np.bitwise_count(mine).sum(axis=1).astype(np.int32)
+    tw = torch.from_numpy(mine.reshape(-1).view(np.int64).copy()).cuda()
+    tc = torch.from_numpy(cards).cuda()
+    distributed.owner_exchange_dedupe(n, tw, tc)  # warm-up (NCCL channels, pools)
+    times, sent, kept = [], 0, 0
+    for _ in range(reps):
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ow, oc, sent = distributed.owner_exchange_dedupe(n, tw, tc)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        kept = oc.numel()
+    ms = max_over_ranks(world, statistics.median(times))
+    total_sent = sum_over_ranks(world, float(sent))
+    return {"rows_per_rank": rows, "ms": ms, "nvlink_bytes_per_rank": sent,
+            "nvlink_bytes_total": total_sent,
+            "nvlink_gbs": total_sent / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "kept_total": sum_over_ranks(world, float(kept)),
+            "note": "device partition + NCCL all_to_all_single (counts, rows, cards) + owner "
+                    "hash dedupe, CUDA events on the current stream, max over ranks"}
+
+
 # ------------------------------------------------------------ cpu baseline
 def reference_sample(spec: str, upper_bound: int, seconds: float):
     """The reference's own engine (oracle/_ref) on a bounded prefix of the
@@ -319,6 +363,11 @@ def run_ours(args, world, rank, local):
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload, R, args.cpu_seconds)
+    if world > 1:
+        try:
+            line["exchange"] = exchange_probe(aut.n, world, rank)
+        except Exception as e:  # the replica numbers above stand on their own
+            line["exchange"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     line["clocks"] = clocks.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
