@@ -534,7 +534,11 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
 }
 
 SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Context* shared) {
-  if (!is_synchronizing(aut)) throw NotSynchronizingError();
+  // Pair merge distances once: the synchronizability precondition
+  // (automaton.hpp:153-157) and Eppstein's bound (heuristics.hpp:26-79) share them.
+  const std::vector<u32> pair_dist = pair_merge_distances(aut, InverseTransitions(aut));
+  if (std::find(pair_dist.begin(), pair_dist.end(), std::numeric_limits<u32>::max()) != pair_dist.end())
+    throw NotSynchronizingError();
   SolveResult res;
   if (aut.state_count() == 1) {
     res.phase = "trivial";
@@ -563,6 +567,7 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
     aopt.cost_fraction = opt.tuning.beam_cost_fraction;
     aopt.set_cost = opt.tuning.cost.set_cost;
     aopt.deadline = Deadline::from_limit(opt.time_limit);
+    aopt.pair_dist = &pair_dist;
     heur = adaptive_upper_bound(aut, aopt, &ctx);
     R = heur->length;
   }

@@ -26,7 +26,10 @@ struct EppsteinStats {
   u32 merge_phases = 0;
 };
 
-EppsteinStats eppstein_with_stats(const Automaton& aut, const Deadline& deadline = {});
+// `dist` (optional): the pair merge distances already computed by the caller
+// (pair_merge_distances, e.g. for the synchronizability check).
+EppsteinStats eppstein_with_stats(const Automaton& aut, const Deadline& deadline = {},
+                                  const std::vector<u32>* dist = nullptr);
 HeuristicResult eppstein(const Automaton& aut, const Deadline& deadline = {});
 
 // Beam inverse BFS keeping the beam_size largest sets per level (card desc,
@@ -38,6 +41,7 @@ struct AdaptiveOptions {
   u64 memory = u64{4} << 30;
   u64 initial_beam = 0;  // 0 -> max(64, n)
   double cost_fraction = 0.05;
+  const std::vector<u32>* pair_dist = nullptr;  // precomputed pair merge distances (optional)
   double set_cost = 512.0;
   Deadline deadline{};
 };
