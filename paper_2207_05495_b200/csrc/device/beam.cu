@@ -325,6 +325,108 @@ __global__ void find_card_kernel(const u32* __restrict__ cards, u64 N, u32 value
 }
 }  // namespace
 
+namespace {
+// 8-bit digit of word w0 at bits [shift, shift+8) — the highest varying bits
+// of the first word in which the rows differ (bits above are constant).
+__global__ void digit_hist_kernel(const u64* __restrict__ words, u64 N, u32 W, u32 w0, u32 shift,
+                                  u32* __restrict__ hist) {
+  __shared__ u32 sh[256];
+  for (u32 i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    atomicAdd(&sh[(words[i * W + w0] >> shift) & 0xFF], 1u);
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void digit_class_kernel(const u64* __restrict__ words, u64 N, u32 W, u32 w0, u32 shift,
+                                   u32 bstar, uint8_t* __restrict__ below, uint8_t* __restrict__ at) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 d = static_cast<u32>((words[i * W + w0] >> shift) & 0xFF);
+    below[i] = d < bstar;
+    at[i] = d == bstar;
+  }
+}
+}  // namespace
+
+// The `need` lexicographically smallest rows of a list of DISTINCT rows, in
+// unspecified order (MSD radix select): each round histograms the 8 highest
+// varying bits of the first varying word, keeps every row of the buckets
+// below the boundary bucket, and recurses into the boundary bucket alone;
+// once the remainder fits one CTA it is sorted and truncated there.
+void select_lex_smallest(Context& c, DList& l, size_t need) {
+  if (l.size() <= need) return;
+  cudaStream_t s = as_stream(c.stream());
+  const u32 W = c.W();
+  std::vector<DList> kept;
+  while (true) {
+    if (need == 0) break;
+    if (l.size() <= need) {
+      kept.push_back(std::move(l));
+      break;
+    }
+    u32 t = 0;
+    if (beam_level_small(c, l, need, &t)) {  // (card desc, lex): cards are equal here
+      kept.push_back(std::move(l));
+      break;
+    }
+    const std::vector<u64> v = varying_bits(c, l);
+    u32 w0 = 0;
+    while (w0 < W && !v[w0]) ++w0;
+    if (w0 == W) {  // all rows equal (cannot happen for distinct rows): keep any `need`
+      truncate(l, need);
+      kept.push_back(std::move(l));
+      break;
+    }
+    const int p = 63 - __builtin_clzll(v[w0]);
+    const u32 shift = static_cast<u32>(p >= 7 ? p - 7 : 0);
+    const u64 N = l.size();
+    auto* hist = static_cast<u32*>(c.scratch(7, 256 * 4));
+    SW_CUDA(cudaMemsetAsync(hist, 0, 256 * 4, s));
+    digit_hist_kernel<<<grid_for(N, 256, 148 * 2), 256, 0, s>>>(l.words, N, W, w0, shift, hist);
+    SW_CHECK_LAUNCH();
+    std::vector<u32> h(256);
+    c.memcpy_d2h(h.data(), hist, 256 * 4);
+    size_t cum = 0;
+    u32 bstar = 0;
+    for (; bstar < 256; ++bstar) {
+      if (cum + h[bstar] >= need) break;
+      cum += h[bstar];
+    }
+    auto* below = static_cast<uint8_t*>(c.alloc(N));
+    auto* at = static_cast<uint8_t*>(c.alloc(N));
+    digit_class_kernel<<<grid_for(N, 256), 256, 0, s>>>(l.words, N, W, w0, shift, bstar, below, at);
+    SW_CHECK_LAUNCH();
+    c.counters.kernel_launches += 3;
+    if (cum) {
+      DList lo = copy_list(c, l, true);
+      compact_flags(c, lo, below, nullptr);
+      kept.push_back(std::move(lo));
+      need -= cum;
+    }
+    compact_flags(c, l, at, nullptr);
+    c.free(below);
+    c.free(at);
+  }
+  size_t total = 0;
+  for (const DList& k : kept) total += k.size();
+  DList out(&c, total, true);
+  size_t off = 0;
+  for (const DList& k : kept) {
+    const size_t cnt = k.size();
+    if (!cnt) continue;
+    SW_CUDA(cudaMemcpyAsync(out.words + off * W, k.words, cnt * W * 8, cudaMemcpyDeviceToDevice, s));
+    SW_CUDA(cudaMemcpyAsync(out.cards + off, k.cards, cnt * 4, cudaMemcpyDeviceToDevice, s));
+    SW_CUDA(cudaMemcpyAsync(out.tags + off, k.tags, cnt * 8, cudaMemcpyDeviceToDevice, s));
+    off += cnt;
+  }
+  out.set_size(total);
+  l = std::move(out);
+}
+
 void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_index) {
   const u32 n = c.n();
   cudaStream_t s = as_stream(c.stream());
@@ -366,13 +468,7 @@ void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_i
     compact_flags(c, a, above, nullptr);
     c.free(above);
     compact_flags(c, l, at, nullptr);
-    if (l.size() > need) {  // one card class of distinct rows: lex order decides
-      u32 t = 0;
-      if (!beam_level_small(c, l, need, &t)) {  // single-CTA sort + truncate when it fits
-        sort_lex(c, l);
-        truncate(l, need);
-      }
-    }
+    select_lex_smallest(c, l, need);  // one card class of distinct rows: lex decides
     DList out(&c, a.size() + l.size(), true);
     const size_t W = c.W();
     for (const DList* src : {&a, &l}) {

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "dev.hpp"
 
@@ -29,5 +30,7 @@ void state_histogram(Context& c, const DList& l, u32* hist);
 // Stable permutation sorting l lexicographically (optionally by descending
 // cardinality first); returned pointer lives in scratch slot 2 or 3.
 const u32* sort_perm(Context& c, const DList& l, bool card_desc);
+// Per word, the bits that are not constant across l (OR ^ AND; one readback).
+std::vector<u64> varying_bits(Context& c, const DList& l);
 
 }  // namespace synchro::dev

@@ -125,6 +125,27 @@ const u32* sort_perm(Context& c, const DList& l, bool card_desc) {
   return vals.Current();
 }
 
+std::vector<u64> varying_bits(Context& c, const DList& l) {
+  const u32 W = c.W();
+  std::vector<unsigned long long> oa(2 * W);
+  for (u32 w = 0; w < W; ++w) {
+    oa[w] = 0;
+    oa[W + w] = ~0ull;
+  }
+  std::vector<u64> out(W, 0);
+  if (l.size() < 2) return out;
+  cudaStream_t s = as_stream(c.stream());
+  auto* d_oa = static_cast<unsigned long long*>(c.scratch(7, 2 * W * 8));
+  c.memcpy_h2d(d_oa, oa.data(), 2 * W * 8);
+  SW_DISPATCH_W(W, {
+    or_and_kernel<W><<<grid_for(l.size(), 256, 148 * 4), 256, 0, s>>>(l.words, l.size(), d_oa);
+  });
+  SW_CHECK_LAUNCH();
+  c.memcpy_d2h(oa.data(), d_oa, 2 * W * 8);
+  for (u32 w = 0; w < W; ++w) out[w] = oa[w] ^ oa[W + w];
+  return out;
+}
+
 void sort_lex(Context& c, DList& l) {
   if (l.size() <= 1) return;
   const u32* perm = sort_perm(c, l, false);
