@@ -430,7 +430,7 @@ void select_lex_smallest(Context& c, DList& l, size_t need) {
 void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_index) {
   const u32 n = c.n();
   cudaStream_t s = as_stream(c.stream());
-  hash_dedupe(c, l);
+  hash_dedupe(c, l, /*first_occurrence=*/false);  // any equal row's tag is a valid parent
   const u64 N = l.size();
   *top_card = 0;
   *top_index = 0;

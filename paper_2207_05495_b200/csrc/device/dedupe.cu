@@ -361,17 +361,21 @@ __device__ __forceinline__ bool claim_one(u32* table, u32 nslots, const u64* __r
 //   C  survivors reserve an output block with one atomicAdd per warp (set
 //      semantics: their order is unspecified) and leave as one block.
 // Rows are read from HBM once.
-template <int W>
+template <int W, bool TAGS>
 __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
-    const u64* __restrict__ words, const u32* __restrict__ cards, u64 N, u32* table, u32 nslots,
-    u32* __restrict__ tile_counter, u64* __restrict__ ow, u32* __restrict__ oc,
-    unsigned long long* __restrict__ out_count) {
+    const u64* __restrict__ words, const u32* __restrict__ cards, const u64* __restrict__ tags,
+    u64 N, u32* table, u32 nslots, u32* __restrict__ tile_counter, u64* __restrict__ ow,
+    u32* __restrict__ oc, u64* __restrict__ ot, unsigned long long* __restrict__ out_count) {
   constexpr int R = rows_per_thread<W>(), T = 32 * R;
   extern __shared__ __align__(16) u64 smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // per warp: rows T*W u64 | cards T u32 | home T u32 | cur T u32 | mine T u32 | pending T u16 | keep T u8
+  //           [| tags T u64, 16-B aligned]
   constexpr int kWarpBytes = T * W * 8 + T * 4 * 4 + T * 2 + T;
-  unsigned char* wbase = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wid) * ((kWarpBytes + 15) & ~15);
+  constexpr int kTagOff = (kWarpBytes + 15) & ~15;
+  constexpr int kStride = TAGS ? kTagOff + T * 8 : kTagOff;
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(smem) + static_cast<size_t>(wid) * kStride;
+  u64* stag = reinterpret_cast<u64*>(wbase + kTagOff);
   u64* srow = reinterpret_cast<u64*>(wbase);
   u32* scard = reinterpret_cast<u32*>(srow + T * W);
   u32* shome = scard + T;
@@ -453,27 +457,33 @@ __global__ void __launch_bounds__(kDdThreads) dd_single_kernel(
 #pragma unroll
         for (int w = 0; w < W; ++w) srow[pos * W + w] = row[j][w];
         scard[pos] = cards[base + j * 32 + lane];
+        if (TAGS) stag[pos] = tags[base + j * 32 + lane];
       }
       off += __popc(bal[j]);
     }
     __syncwarp();
     u64* dst = ow + excl * W;
     for (u32 e = lane; e < agg * W; e += 32) __stcs(dst + e, srow[e]);
-    for (u32 e = lane; e < agg; e += 32) __stcs(oc + excl + e, scard[e]);
+    for (u32 e = lane; e < agg; e += 32) {
+      __stcs(oc + excl + e, scard[e]);
+      if (TAGS) __stcs(ot + excl + e, stag[e]);
+    }
     __syncwarp();
   }
 }
 
-template <int W>
+template <int W, bool TAGS>
 constexpr size_t single_warp_bytes() {
   constexpr int T = 32 * rows_per_thread<W>();
-  return (static_cast<size_t>(T) * W * 8 + T * 4 * 4 + T * 2 + T + 15) & ~size_t{15};
+  return ((static_cast<size_t>(T) * W * 8 + T * 4 * 4 + T * 2 + T + 15) & ~size_t{15}) +
+         (TAGS ? static_cast<size_t>(T) * 8 : 0);
 }
 
 }  // namespace
 
 template <int W>
 static size_t hash_dedupe_single(Context& c, DList& l) {
+  const bool tagged = l.tagged();
   constexpr int T = rows_per_thread<W>() * 32;  // rows per warp tile
   const u64 N = l.size();
   cudaStream_t s = as_stream(c.stream());
@@ -486,14 +496,16 @@ static size_t hash_dedupe_single(Context& c, DList& l) {
   auto* aux = static_cast<u64*>(c.scratch(6, 16));  // [tile counter, output count]
   SW_CUDA(cudaMemsetAsync(table, 0, static_cast<size_t>(nslots) * 4, s));
   SW_CUDA(cudaMemsetAsync(aux, 0, 16, s));
-  const size_t smem = static_cast<size_t>(kDdThreads / 32) * single_warp_bytes<W>();
-  smem_opt_in(reinterpret_cast<const void*>(dd_single_kernel<W>), static_cast<int>(smem));
-  DList out(&c, N, false);
+  const size_t smem = static_cast<size_t>(kDdThreads / 32) *
+                      (tagged ? single_warp_bytes<W, true>() : single_warp_bytes<W, false>());
+  auto kern = tagged ? dd_single_kernel<W, true> : dd_single_kernel<W, false>;
+  smem_opt_in(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
+  DList out(&c, N, tagged);
   const unsigned grid = static_cast<unsigned>(
       std::min<u64>((ntiles + kDdThreads / 32 - 1) / (kDdThreads / 32), 148 * 8));
-  dd_single_kernel<W><<<grid, kDdThreads, smem, s>>>(
-      l.words, l.cards, N, table, nslots, reinterpret_cast<u32*>(aux), out.words, out.cards,
-      reinterpret_cast<unsigned long long*>(aux + 1));
+  kern<<<grid, kDdThreads, smem, s>>>(l.words, l.cards, l.tags, N, table, nslots,
+                                     reinterpret_cast<u32*>(aux), out.words, out.cards, out.tags,
+                                     reinterpret_cast<unsigned long long*>(aux + 1));
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
   u64 kept = 0;
@@ -541,14 +553,14 @@ static size_t hash_dedupe_tiled(Context& c, DList& l) {
   return N - kept;
 }
 
-size_t hash_dedupe(Context& c, DList& l) {
+size_t hash_dedupe(Context& c, DList& l, bool first_occurrence) {
   const u64 N = l.size();
   if (N <= 1) return 0;
   // index does not fit 25 bits (SYNCHRO_DEDUPE_WIDE=1 forces this path: tests)
   const char* wide = std::getenv("SYNCHRO_DEDUPE_WIDE");
   if (N >= kIdxMask || (wide && *wide == '1')) return hash_dedupe_wide(c, l);
   size_t r = 0;
-  if (l.tagged()) {  // tags differ between equal rows: the minimum index must win
+  if (l.tagged() && first_occurrence) {  // tags differ between equal rows: the minimum index must win
     SW_DISPATCH_W(c.W(), { r = hash_dedupe_tiled<W>(c, l); });
   } else {
     SW_DISPATCH_W(c.W(), { r = hash_dedupe_single<W>(c, l); });

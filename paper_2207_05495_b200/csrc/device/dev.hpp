@@ -174,7 +174,9 @@ size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
 // distinct value, survivors in UNSPECIFIED order (callers are order-free).
 // Tagged lists keep the first occurrence's tag (minimum index, the
 // reference's survivor).  Returns #removed.
-size_t hash_dedupe(Context& c, DList& l);
+// first_occurrence=false (tagged lists): any occurrence's tag may survive — every
+// equal row's tag names a valid parent, so reconstructed words stay valid; one pass.
+size_t hash_dedupe(Context& c, DList& l, bool first_occurrence = true);
 // Hash ownership (exchange.cu): regroups l owner-major by owner = h(row) mod
 // nranks (order inside an owner's segment unspecified); returns the rows per owner.
 std::vector<u64> owner_partition(Context& c, DList& l, u32 nranks);

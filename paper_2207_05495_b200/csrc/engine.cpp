@@ -193,7 +193,7 @@ void GpuBibfs::bfs_step(bool with_history) {
   // Set-semantics dedupe (hash; same survivors as the reference's stable lex
   // sort + unique).  L_BFS needs no lex order: every consumer either sorts its
   // own relabelled copy (containment index) or is order-free (stats, ledger).
-  const double r_dupl = generated ? ratio(dev::hash_dedupe(ctx_, next), generated) : 0.0;
+  const double r_dupl = generated ? ratio(dev::hash_dedupe(ctx_, next, /*first_occurrence=*/false), generated) : 0.0;
   const size_t after_dupl = next.size();
   const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
   double r_hist = 0.0;
@@ -387,7 +387,8 @@ class DfsRunner {
     // the dedupe is set-semantic (first occurrence survives, as after the
     // stable sort), and the trie query is order-free.
     bool sorted = false;
-    if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0) dev::hash_dedupe(c_, next);
+    if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0)
+      dev::hash_dedupe(c_, next, /*first_occurrence=*/false);  // any equal row's tag is a valid parent
     if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
       // Drop sets that are proper subsets of one of the dfs_largest first
       // (largest) sets.  The reference marks proper supersets among
