@@ -357,7 +357,7 @@ __global__ void digit_class_kernel(const u64* __restrict__ words, u64 N, u32 W, 
 // varying bits of the first varying word, keeps every row of the buckets
 // below the boundary bucket, and recurses into the boundary bucket alone;
 // once the remainder fits one CTA it is sorted and truncated there.
-void select_lex_smallest(Context& c, DList& l, size_t need) {
+void select_lex_smallest(Context& c, DList& l, size_t need, bool distinct) {
   if (l.size() <= need) return;
   cudaStream_t s = as_stream(c.stream());
   const u32 W = c.W();
@@ -369,14 +369,14 @@ void select_lex_smallest(Context& c, DList& l, size_t need) {
       break;
     }
     u32 t = 0;
-    if (beam_level_small(c, l, need, &t)) {  // (card desc, lex): cards are equal here
+    if (distinct && beam_level_small(c, l, need, &t)) {  // (card desc, lex): cards equal here
       kept.push_back(std::move(l));
       break;
     }
     const std::vector<u64> v = varying_bits(c, l);
     u32 w0 = 0;
     while (w0 < W && !v[w0]) ++w0;
-    if (w0 == W) {  // all rows equal (cannot happen for distinct rows): keep any `need`
+    if (w0 == W) {  // all remaining rows equal (only with duplicates): any `need` copies
       truncate(l, need);
       kept.push_back(std::move(l));
       break;
@@ -402,7 +402,7 @@ void select_lex_smallest(Context& c, DList& l, size_t need) {
     SW_CHECK_LAUNCH();
     c.counters.kernel_launches += 3;
     if (cum) {
-      DList lo = copy_list(c, l, true);
+      DList lo = copy_list(c, l, l.tagged());
       compact_flags(c, lo, below, nullptr);
       kept.push_back(std::move(lo));
       need -= cum;
@@ -413,14 +413,15 @@ void select_lex_smallest(Context& c, DList& l, size_t need) {
   }
   size_t total = 0;
   for (const DList& k : kept) total += k.size();
-  DList out(&c, total, true);
+  const bool tagged = l.tagged();
+  DList out(&c, total, tagged);
   size_t off = 0;
   for (const DList& k : kept) {
     const size_t cnt = k.size();
     if (!cnt) continue;
     SW_CUDA(cudaMemcpyAsync(out.words + off * W, k.words, cnt * W * 8, cudaMemcpyDeviceToDevice, s));
     SW_CUDA(cudaMemcpyAsync(out.cards + off, k.cards, cnt * 4, cudaMemcpyDeviceToDevice, s));
-    SW_CUDA(cudaMemcpyAsync(out.tags + off, k.tags, cnt * 8, cudaMemcpyDeviceToDevice, s));
+    if (tagged) SW_CUDA(cudaMemcpyAsync(out.tags + off, k.tags, cnt * 8, cudaMemcpyDeviceToDevice, s));
     off += cnt;
   }
   out.set_size(total);
@@ -468,7 +469,7 @@ void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_i
     compact_flags(c, a, above, nullptr);
     c.free(above);
     compact_flags(c, l, at, nullptr);
-    select_lex_smallest(c, l, need);  // one card class of distinct rows: lex decides
+    select_lex_smallest(c, l, need, /*distinct=*/true);  // one card class: lex decides
     DList out(&c, a.size() + l.size(), true);
     const size_t W = c.W();
     for (const DList* src : {&a, &l}) {
@@ -494,6 +495,56 @@ void beam_select(Context& c, DList& l, size_t beam, u32* top_card, size_t* top_i
     *top_index = static_cast<size_t>(pos);
     c.counters.kernel_launches += 1;
   }
+}
+
+// The first k rows of l in (card desc, lex) order — as a multiset, duplicates
+// counted like the reference's slice of its sorted level (dfs_phase.hpp:107-110)
+// — without sorting l: card histogram → boundary card → radix select inside the
+// boundary class.  Untagged copy, unspecified order; l is untouched.
+DList top_card_desc_lex(Context& c, const DList& l, size_t k) {
+  const u32 n = c.n();
+  const u64 N = l.size();
+  cudaStream_t s = as_stream(c.stream());
+  if (N <= k) return copy_list(c, l, false);
+  auto* hist = static_cast<u32*>(c.scratch(7, (static_cast<size_t>(n) + 1) * 4));
+  SW_CUDA(cudaMemsetAsync(hist, 0, (static_cast<size_t>(n) + 1) * 4, s));
+  card_hist_kernel<<<grid_for(N, 256, 148 * 2), 256, (n + 1) * 4, s>>>(l.cards, N, n, hist);
+  SW_CHECK_LAUNCH();
+  std::vector<u32> h(n + 1);
+  c.memcpy_d2h(h.data(), hist, (static_cast<size_t>(n) + 1) * 4);
+  u64 cum = 0;
+  u32 cs = 0;
+  for (u32 v = n + 1; v-- > 0;) {
+    if (cum + h[v] >= k) {
+      cs = v;
+      break;
+    }
+    cum += h[v];
+  }
+  auto* above = static_cast<uint8_t*>(c.alloc(N));
+  auto* at = static_cast<uint8_t*>(c.alloc(N));
+  card_class_kernel<<<grid_for(N, 256), 256, 0, s>>>(l.cards, N, cs, above, at);
+  SW_CHECK_LAUNCH();
+  DList a = copy_list(c, l, false);
+  compact_flags(c, a, above, nullptr);
+  DList e = copy_list(c, l, false);
+  compact_flags(c, e, at, nullptr);
+  c.free(above);
+  c.free(at);
+  select_lex_smallest(c, e, k - cum, /*distinct=*/false);
+  const size_t W = c.W();
+  DList out(&c, a.size() + e.size(), false);
+  if (a.size()) {
+    c.memcpy_d2d(out.words, a.words, a.size() * W * 8);
+    c.memcpy_d2d(out.cards, a.cards, a.size() * 4);
+  }
+  if (e.size()) {
+    c.memcpy_d2d(out.words + a.size() * W, e.words, e.size() * W * 8);
+    c.memcpy_d2d(out.cards + a.size(), e.cards, e.size() * 4);
+  }
+  out.set_size(a.size() + e.size());
+  c.counters.kernel_launches += 2;
+  return out;
 }
 
 }  // namespace synchro::dev

@@ -259,8 +259,11 @@ bool beam_level_small(Context& c, DList& next, size_t beam, u32* top_card);
 // truncate(beam), in unspecified order (beam.cu): *top_card = max kept card,
 // *top_index = the position of Q in `next` when *top_card == n.
 void beam_select(Context& c, DList& next, size_t beam, u32* top_card, size_t* top_index);
-// The `need` lex-smallest rows of a tagged list of distinct rows, in unspecified order.
-void select_lex_smallest(Context& c, DList& l, size_t need);
+// The `need` lex-smallest rows of l, in unspecified order (distinct: l has no
+// duplicates — enables the single-CTA finish, which dedupes).
+void select_lex_smallest(Context& c, DList& l, size_t need, bool distinct);
+// First k rows of l in (card desc, lex) order as a multiset (untagged copy, any order).
+DList top_card_desc_lex(Context& c, const DList& l, size_t k);
 // The whole beam search (from the singletons, at most level_cap levels) in one
 // single-CTA launch when the beam fits shared memory.  Found: *word = the reset
 // word (first letter first); NotFound: no word within level_cap;

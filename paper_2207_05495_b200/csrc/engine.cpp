@@ -382,20 +382,19 @@ class DfsRunner {
     expansions += static_cast<u64>(hi - lo) * k;
     const u64 generated = next.size();
     // The reference sorts every level by (card desc, lex, index) (dfs_phase.hpp:105).
-    // The order is observable only through the top-dfs_largest window and the
-    // slice boundaries, so it is materialised only when one of those happens;
-    // the dedupe is set-semantic (first occurrence survives, as after the
-    // stable sort), and the trie query is order-free.
-    bool sorted = false;
+    // The order is observable only through the top-dfs_largest window (selected
+    // as a multiset without sorting) and the slice boundaries (sorted only when the
+    // level is sliced); the dedupe is set-semantic (which equal row's tag survives
+    // changes only the reported witness), and the trie query is order-free.
     if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0)
       dev::hash_dedupe(c_, next, /*first_occurrence=*/false);  // any equal row's tag is a valid parent
     if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
       // Drop sets that are proper subsets of one of the dfs_largest first
       // (largest) sets.  The reference marks proper supersets among
       // complements; on plain sets it is a superset join (order kept).
-      dev::sort_card_desc_lex(c_, next);
-      sorted = true;
-      const DList largest = dev::slice_copy(c_, next, 0, t_.dfs_largest, false);
+      // The window is the first dfs_largest rows of the sorted level (a multiset);
+      // selected without sorting the level (beam.cu top_card_desc_lex).
+      const DList largest = dev::top_card_desc_lex(c_, next, t_.dfs_largest);
       dev::remove_subsets_of(c_, largest, next, /*proper=*/true);
     }
     const u64 now = list_footprint(n, next.size());
@@ -416,7 +415,7 @@ class DfsRunner {
     }
     if (r >= bound_ - 1) return;
     const size_t cap = slice_cap(r);
-    if (next.size() > cap && !sorted) dev::sort_card_desc_lex(c_, next);  // slices follow the order
+    if (next.size() > cap) dev::sort_card_desc_lex(c_, next);  // slices follow the order
     const Frame frame{parent, &next};
     for (size_t plo = 0; plo < next.size(); plo += cap) {
       recurse(next, plo, std::min(next.size(), plo + cap), r + 1, level + 1, &frame);
