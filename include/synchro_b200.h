@@ -72,6 +72,14 @@ typedef struct sw_solve_options {
   uint32_t dfs_shard_index; /* multi-GPU DFS partition: this process's share ... */
   uint32_t dfs_shard_count; /* ... of L_IBFS (threshold = MIN over shards); 1 = whole */
   int32_t contain_stats;    /* 1: count containment-traversal node visits / pair tests */
+  /* EngineTuning / TuningParams fields beyond the CLI's (bibfs_engine.hpp:27-37,
+   * cost_model.hpp:26-36); semantic: they change the schedule, DFS sizes or R. */
+  uint64_t dfs_largest;        /* 20000: DFS window (dfs_phase.hpp:18) */
+  double history_growth;       /* 2.0: prune a history once it has grown this much */
+  uint64_t beam_initial;       /* 0: max(64, n) (heuristics.hpp:144-150) */
+  double beam_cost_fraction;   /* 0.05 */
+  double reduction_of_reduction; /* <= 0: unset (1/k) */
+  uint64_t stop_after_iterations; /* analysis: stop after this many iterations (0: never) */
 } sw_solve_options;
 
 /* SolveResult (bibfs_engine.hpp:50-59) + expansion counters and timings. */
@@ -91,7 +99,7 @@ typedef struct sw_solve_result {
   double engine_seconds;
   double expand_kernel_ms;
   uint64_t kernel_launches;
-  char phase[16];           /* "meet" | "dfs" | "bound" | "trivial" */
+  char phase[16];           /* "meet" | "dfs" | "bound" | "trivial" | "stopped" */
   double engine_device_ms;  /* CUDA-event span of the engine on its stream */
   uint64_t h2d_bytes;       /* host->device bytes copied during the solve */
   uint64_t d2h_bytes;       /* device->host bytes copied during the solve */
@@ -124,6 +132,14 @@ int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, const uint32
 int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta, const sw_solve_options* opt,
                    sw_solve_result* result, uint32_t* word, size_t word_cap,
                    const char* trace_path);
+/* Same, plus the DFS level log: one record {r, level, in, generated, kept} per
+ * recurse() call in call order (dfs_phase.hpp:82-159), up to dfs_levels_cap
+ * records into dfs_levels[5*i..5*i+4]; *dfs_levels_count = records produced
+ * (may exceed the cap). */
+int sw_solve_exact_ex(uint32_t n, uint32_t k, const uint32_t* delta, const sw_solve_options* opt,
+                      sw_solve_result* result, uint32_t* word, size_t word_cap,
+                      const char* trace_path, uint64_t* dfs_levels, size_t dfs_levels_cap,
+                      size_t* dfs_levels_count);
 
 /* ---- heuristics (heuristics.hpp:26-184) ----
  * algorithm: 0 eppstein, 1 beam, 2 adaptive.  Returns SW_ERR_REFUSED when the
@@ -196,6 +212,13 @@ int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count, const uint
                  size_t b_count, int32_t mode, uint8_t* keep);
 int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
                        const uint64_t* b_words, size_t b_count, int32_t* met);
+/* Host-side (no device): the order in which the reference's meet_check
+ * (subset_algebra.hpp:201-210) leaves b when it finds no containment:
+ * order[p] = original index of the element now at position p.  a must be
+ * lex-sorted unique (else SW_ERR_PARSE); min_brute as EngineTuning. */
+int sw_meet_check_order(uint32_t n, const uint64_t* a_words, size_t a_count,
+                        const uint64_t* b_words, size_t b_count, uint32_t min_brute,
+                        uint32_t* order);
 /* Node count of the reference StaticTrie over a duplicate-free list. */
 /* ---- cost model (cost_model.hpp:67-250), host-side doubles ---- */
 double sw_exp_mark(double a_size, double b_size, double a_density, double b_density);

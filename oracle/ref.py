@@ -38,6 +38,12 @@ class RefOptions(C.Structure):
         ("dedupe_cadence", C.c_uint32),
         ("reduce_cadence", C.c_uint32),
         ("max_seconds", C.c_double),
+        ("dfs_largest", C.c_uint64),
+        ("history_growth", C.c_double),
+        ("beam_initial", C.c_uint64),
+        ("beam_cost_fraction", C.c_double),
+        ("reduction_of_reduction", C.c_double),
+        ("stop_after_iterations", C.c_uint64),
     ]
 
 
@@ -66,7 +72,9 @@ def default_options(**kw) -> RefOptions:
     o = RefOptions(
         memory=4 << 30, time_limit=0.0, track_word=0, schedule=0, upper_bound=0,
         set_cost=512.0, dfs_set_weight=0.25, dfs_check_weight=0.25, min_brute=64,
-        min_leaf=10, dedupe_cadence=2, reduce_cadence=3, max_seconds=0.0)
+        min_leaf=10, dedupe_cadence=2, reduce_cadence=3, max_seconds=0.0, dfs_largest=20000,
+        history_growth=2.0, beam_initial=0, beam_cost_fraction=0.05, reduction_of_reduction=0.0,
+        stop_after_iterations=0)
     for k, v in kw.items():
         if k == "schedule" and isinstance(v, str):
             v = SCHEDULES[v]
@@ -111,6 +119,8 @@ def lib():
         L.ref_mark.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t, C.c_int, _u8p]
         L.ref_mark.restype = C.c_size_t
         L.ref_meet_check.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t]
+        L.ref_meet_check_order.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
+                                           C.c_uint32, _u32p]
         L.ref_trie_node_count.argtypes = [C.c_uint32, _u64p, C.c_size_t, C.c_uint32,
                                           C.POINTER(C.c_uint64)]
         L.ref_trie_node_count.restype = C.c_uint64
@@ -251,6 +261,15 @@ def meet_check(n, a_words, b_words) -> bool:
     a = np.ascontiguousarray(a_words, np.uint64)
     b = np.ascontiguousarray(b_words, np.uint64).copy()
     return bool(lib().ref_meet_check(n, a, a.size // W(n), b, b.size // W(n)))
+
+
+def meet_check_order(n, a_words, b_words, min_brute=64):
+    """(met, order): the order meet_check leaves b in (order[p] = original index)."""
+    a = np.ascontiguousarray(a_words, np.uint64)
+    b = np.ascontiguousarray(b_words, np.uint64)
+    order = np.zeros(b.size // W(n), np.uint32)
+    met = lib().ref_meet_check_order(n, a, a.size // W(n), b, b.size // W(n), min_brute, order)
+    return bool(met), order
 
 
 def trie_node_count(n, words, min_leaf=10):

@@ -258,6 +258,20 @@ REF_API int ref_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
   return meet_check(a, b) ? 1 : 0;
 }
 
+// The order the reference's meet_check (subset_algebra.hpp:201-210) leaves b
+// in: order[p] = original index of the element at position p.  Returns met.
+REF_API int ref_meet_check_order(uint32_t n, const uint64_t* a_words, size_t a_count,
+                                 const uint64_t* b_words, size_t b_count, uint32_t min_brute,
+                                 uint32_t* order) {
+  SetList a = list_from(n, a_words, nullptr, nullptr, a_count);
+  SetList b = list_from(n, b_words, nullptr, nullptr, b_count);
+  SetList bt(n, true);
+  for (size_t j = 0; j < b_count; ++j) bt.push_back_view(b.view(j), j);
+  const bool met = meet_check(a, bt, {min_brute});
+  for (size_t j = 0; j < b_count; ++j) order[j] = static_cast<uint32_t>(bt.tag(j));
+  return met ? 1 : 0;
+}
+
 // Static trie over a duplicate-free list: node count and ledger footprint
 // (static_trie.hpp:26-45); also answers a joint query for `q` if given.
 REF_API uint64_t ref_trie_node_count(uint32_t n, const uint64_t* words, size_t count,
@@ -307,6 +321,14 @@ struct RefOptions {
   uint32_t dedupe_cadence;
   uint32_t reduce_cadence;
   double max_seconds;   // instrumented replay only: stop between iterations (bounded CPU sample)
+  // EngineTuning / TuningParams fields beyond the CLI's (bibfs_engine.hpp:27-37,
+  // cost_model.hpp:26-36)
+  uint64_t dfs_largest;
+  double history_growth;
+  uint64_t beam_initial;
+  double beam_cost_fraction;
+  double reduction_of_reduction;  // <= 0: unset (1/k)
+  uint64_t stop_after_iterations; // instrumented replay only: 0 = none
 };
 
 struct RefResult {
@@ -341,6 +363,11 @@ SolveOptions to_solve_options(const RefOptions& o) {
   s.tuning.min_leaf = o.min_leaf;
   s.tuning.dfs_dedupe_cadence = o.dedupe_cadence;
   s.tuning.dfs_reduce_cadence = o.reduce_cadence;
+  s.tuning.dfs_largest = o.dfs_largest;
+  s.tuning.history_growth = o.history_growth;
+  s.tuning.beam_initial = o.beam_initial;
+  s.tuning.beam_cost_fraction = o.beam_cost_fraction;
+  if (o.reduction_of_reduction > 0) s.tuning.cost.dfs_reduction_of_reduction = o.reduction_of_reduction;
   return s;
 }
 
@@ -523,7 +550,10 @@ REF_API int ref_solve_instrumented(uint32_t n, uint32_t k, const uint32_t* delta
   try {
     const Automaton aut = make_aut(n, k, delta);
     SolveOptions opt = to_solve_options(*o);
-    opt.track_word = false;
+    // With track_word the reference meets through meet_find on a copy
+    // (L_IBFS keeps its committed order); without, meet_check permutes L_IBFS
+    // in place (subset_algebra.hpp:201-219) -- the DFS's top-level slices follow
+    // that order, so the replay keeps the distinction.
     opt.trace = tr;
     if (!is_synchronizing(aut)) throw NotSynchronizingError();
     if (n == 1) return 0;
@@ -556,6 +586,11 @@ REF_API int ref_solve_instrumented(uint32_t n, uint32_t k, const uint32_t* delta
       if (o->max_seconds > 0 &&
           std::chrono::duration<double>(std::chrono::steady_clock::now() - te).count() >
               o->max_seconds) {
+        done(0);
+        res->status = 7;
+        return 7;
+      }
+      if (o->stop_after_iterations && res->iterations >= o->stop_after_iterations) {
         done(0);
         res->status = 7;
         return 7;
@@ -628,7 +663,7 @@ REF_API int ref_solve_instrumented(uint32_t n, uint32_t k, const uint32_t* delta
       else
         ++res->ibfs_steps;
       detail::trace_line(tr, eng, st, sc, kind);
-      if (eng.meet()) {
+      if (opt.track_word ? eng.meet_witness().has_value() : eng.meet()) {
         if (tr) *tr << "result=" << r << " phase=meet\n";
         return done(r);
       }

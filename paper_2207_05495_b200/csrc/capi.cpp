@@ -12,6 +12,7 @@
 #include "device/dev.hpp"
 #include "engine.hpp"
 #include "experiment.hpp"
+#include "meet_order.hpp"
 
 #define SW_EXPORT extern "C" __attribute__((visibility("default")))
 
@@ -89,6 +90,12 @@ SolveOptions to_options(const sw_solve_options* o) {
   s.tuning.min_leaf = o->min_leaf;
   s.tuning.dfs_dedupe_cadence = o->dedupe_cadence;
   s.tuning.dfs_reduce_cadence = o->reduce_cadence;
+  s.tuning.dfs_largest = o->dfs_largest;
+  s.tuning.history_growth = o->history_growth;
+  s.tuning.beam_initial = o->beam_initial;
+  s.tuning.beam_cost_fraction = o->beam_cost_fraction;
+  if (o->reduction_of_reduction > 0) s.tuning.cost.dfs_reduction_of_reduction = o->reduction_of_reduction;
+  s.stop_after_iterations = o->stop_after_iterations;
   s.device = o->device;
   s.timing = o->timing != 0;
   s.contain_stats = o->contain_stats != 0;
@@ -132,6 +139,12 @@ SW_EXPORT void sw_default_options(sw_solve_options* o) {
   o->device = -1;
   o->dfs_shard_index = 0;
   o->dfs_shard_count = 1;
+  o->dfs_largest = 20000;
+  o->history_growth = 2.0;
+  o->beam_initial = 0;
+  o->beam_cost_fraction = 0.05;
+  o->reduction_of_reduction = 0.0;
+  o->stop_after_iterations = 0;
 }
 
 SW_EXPORT int sw_random_automaton(uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta_out) {
@@ -179,7 +192,15 @@ SW_EXPORT int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, co
 SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
                              const sw_solve_options* o, sw_solve_result* out, uint32_t* word,
                              size_t word_cap, const char* trace_path) {
+  return sw_solve_exact_ex(n, k, delta, o, out, word, word_cap, trace_path, nullptr, 0, nullptr);
+}
+
+SW_EXPORT int sw_solve_exact_ex(uint32_t n, uint32_t k, const uint32_t* delta,
+                                const sw_solve_options* o, sw_solve_result* out, uint32_t* word,
+                                size_t word_cap, const char* trace_path, uint64_t* dfs_levels,
+                                size_t dfs_levels_cap, size_t* dfs_levels_count) {
   return guarded([&] {
+    if (dfs_levels_count) *dfs_levels_count = 0;
     std::memset(out, 0, sizeof(*out));
     const Automaton aut = make_aut(n, k, delta);
     SolveOptions opt = to_options(o);
@@ -215,6 +236,10 @@ SW_EXPORT int sw_solve_exact(uint32_t n, uint32_t k, const uint32_t* delta,
     std::strncpy(out->phase, r.phase.c_str(), sizeof(out->phase) - 1);
     if (r.word && word)
       for (size_t i = 0; i < r.word->size() && i < word_cap; ++i) word[i] = (*r.word)[i];
+    if (dfs_levels_count) *dfs_levels_count = r.dfs_levels.size();
+    if (dfs_levels)
+      for (size_t i = 0; i < r.dfs_levels.size() && i < dfs_levels_cap; ++i)
+        for (int f = 0; f < 5; ++f) dfs_levels[5 * i + f] = r.dfs_levels[i][f];
   });
 }
 
@@ -477,6 +502,21 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
     const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
     *met = dev::exists_subset(c, ix, b, nullptr) ? 1 : 0;
+  });
+}
+
+SW_EXPORT int sw_meet_check_order(uint32_t n, const uint64_t* a_words, size_t a_count,
+                                  const uint64_t* b_words, size_t b_count, uint32_t min_brute,
+                                  uint32_t* order) {
+  if (!sorted_unique(a_words, a_count, words_for(n))) {
+    g_last_error = "meet_check: first list must be lex-sorted and unique";
+    return SW_ERR_PARSE;
+  }
+  return guarded([&] {
+    std::vector<u32> ord(b_count);
+    for (size_t i = 0; i < b_count; ++i) ord[i] = static_cast<u32>(i);
+    detail::replay_meet_check(a_words, a_count, b_words, words_for(n), n, min_brute, ord);
+    std::memcpy(order, ord.data(), b_count * 4);
   });
 }
 

@@ -21,7 +21,9 @@
 // traversal order, so sizes match the reference bit-exactly.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "dev.hpp"
 #include "kernels.cuh"
@@ -306,7 +308,7 @@ template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_kernel(
     const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
     u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
-    u32* overflow_scans, unsigned long long* stats, const u64* __restrict__ andm) {
+    u32* overflow_scans, unsigned long long* stats, const u64* __restrict__ andm, u32 spill_cap) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
     const unsigned m0 = __ballot_sync(FULL, c0 != kNone);
     const unsigned m1 = __ballot_sync(FULL, c1 != kNone);
     const int n0 = __popc(m0), n1 = __popc(m1);
-    if (sp + n0 + n1 > kPoolCap && gsp + kSpill <= kSpillCap) {
+    if (sp + n0 + n1 > kPoolCap && gsp + kSpill <= static_cast<int>(spill_cap)) {
       // spill the oldest kSpill tasks; sp <= kPoolCap = 2 kSpill, so the
       // shifted block [kSpill, sp) and its target [0, sp - kSpill) are disjoint
       for (int i = lane; i < kSpill; i += 32)
@@ -527,7 +529,13 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
       sp -= kSpill;
     }
     if (sp + n0 + n1 > kPoolCap) {
-      if (c0 != kNone) brute = true;  // pool and spill full: scan the opened range
+      // Pool and spill stack full: scan the opened range instead of descending.
+      // An internal-node task loaded only query words d/64, d/64+1 (a long run
+      // loaded the whole row): the scan needs all of y.
+      if (c0 != kNone) {
+        if (!longrun) load_row<W>(B, j, y, ycard);
+        brute = true;
+      }
       if (lane == 0) atomicAdd(overflow_scans, 1u);
     } else {
       if (c1 != kNone) {
@@ -649,6 +657,13 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   }
   uint4* spill = static_cast<uint4*>(
       c.scratch(10, static_cast<size_t>(grid) * kPoolWarps * kSpillCap * sizeof(uint4)));
+  // Test hook: SYNCHRO_SPILL_CAP (tasks per warp, <= kSpillCap) shrinks the
+  // spill stack so the overflow scan path runs (tests/test_gpu_primitives.py).
+  const u32 spill_cap = [] {
+    const char* e = std::getenv("SYNCHRO_SPILL_CAP");
+    const long v = e && *e ? std::strtol(e, nullptr, 10) : kSpillCap;
+    return static_cast<u32>(std::clamp<long>(v, 0, kSpillCap));
+  }();
   std::unique_ptr<StreamTimer> timer;
   if (progress_enabled() || c.timing) {
     timer = std::make_unique<StreamTimer>(c);
@@ -658,7 +673,7 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
         p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
         static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1, stats,
-        static_cast<const u64*>(p.tree.andmask));
+        static_cast<const u64*>(p.tree.andmask), spill_cap);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;

@@ -248,6 +248,8 @@ DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged);
 DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool tagged);
 // h := sorted merge of disjoint lex-sorted unique lists h and add (untagged).
 void merge_sorted(Context& c, DList& h, const DList& add);
+// l := rows perm[0], perm[1], ... of l (perm: device array of l.size() indices).
+void gather_rows(Context& c, DList& l, const u32* perm);
 u64 read_tag(Context& c, const DList& l, size_t i);
 std::vector<u64> read_tags(Context& c, const DList& l);
 
@@ -273,6 +275,18 @@ BeamRun beam_full_small(Context& c, size_t beam, u64 level_cap, std::vector<u32>
 
 // ---- static trie shape (static_trie.hpp:85-151) for exact ledger accounting
 u64 trie_node_count(Context& c, const DList& l, u32 min_leaf);
+// The same construction, recording the internal nodes round by round (root =
+// rounds[0][0]; no rounds when the whole list is one leaf): division state,
+// min cardinality and the internal children as indices into the next round
+// (0xFFFFFFFF: a leaf / absorbed payload).  Returns the node count.
+struct TrieShape {
+  struct Node {
+    u32 div, min_card, zero, one;
+  };
+  u32 min_leaf = 10;
+  std::vector<std::vector<Node>> rounds;
+};
+u64 trie_shape(Context& c, const DList& l, u32 min_leaf, TrieShape* shape);
 
 // ---- microbenchmarks (microbench.cu): avg CUDA-event ms per call on `count`
 // device-generated random sets of the given density.

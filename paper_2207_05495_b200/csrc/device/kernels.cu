@@ -8,80 +8,6 @@
 
 namespace synchro::dev {
 
-// ---------------------------------------------------------------- expansion
-// One thread per parent set; the parent is read once and all k children are
-// produced from it (the reference's compute_layer i×a loop,
-// bibfs_engine.hpp:350-364, fused over letters).  Work is proportional to
-// |S| (scatter over set bits), not to n: image sets bit delta(q,a) for each
-// q in S; preimage sets the CSR row delta^-1(q,a) (mean in-degree 1).  The
-// tables (<= 24 KB) are staged in shared memory.
-template <int W, bool INV>
-__global__ void __launch_bounds__(256) expand_kernel(
-    const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
-    const uint16_t* __restrict__ g_img, const u32* __restrict__ g_off,
-    const uint16_t* __restrict__ g_src, u64* __restrict__ out, u32* __restrict__ out_card,
-    u64* __restrict__ out_tag) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const u32 kn = k * n;
-  u32* s_off = reinterpret_cast<u32*>(smem);
-  uint16_t* s_tab = INV ? reinterpret_cast<uint16_t*>(s_off + kn + 1)
-                        : reinterpret_cast<uint16_t*>(smem);
-  if (INV) {
-    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_src[i];
-  } else {
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
-  }
-  __syncthreads();
-
-  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
-    u64 s[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) s[w] = __ldg(src + (lo + i) * W + w);
-    for (u32 a = 0; a < k; ++a) {
-      u64 acc[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) acc[w] = 0;
-      const u32 base = a * n;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        u64 bits = s[w];
-        while (bits) {
-          const int b = __clzll(bits);
-          bits &= ~(u64{1} << (63 - b));
-          const u32 q = static_cast<u32>(w * 64 + b);
-          if (!INV) {
-            const u32 t = s_tab[base + q];
-            const u64 m = u64{1} << (63 - (t & 63));
-            const u32 tw = t >> 6;
-#pragma unroll
-            for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == tw) ? m : 0;
-          } else {
-            const u32 e1 = s_off[base + q + 1];
-            for (u32 e = s_off[base + q]; e < e1; ++e) {
-              const u32 t = s_tab[e];
-              const u64 m = u64{1} << (63 - (t & 63));
-              const u32 tw = t >> 6;
-#pragma unroll
-              for (int x = 0; x < W; ++x) acc[x] |= (static_cast<u32>(x) == tw) ? m : 0;
-            }
-          }
-        }
-      }
-      const u64 o = i * k + a;
-      u32 c = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        out[o * W + w] = acc[w];
-        c += __popcll(acc[w]);
-      }
-      out_card[o] = c;
-      if (out_tag) out_tag[o] = ((lo + i) << 16) | a;
-    }
-  }
-}
-
 // ------------------------------------------------------ bit-sliced expansion
 // A warp takes 64 parents at a time and transposes them into per-state bit
 // slices (slice[q] bit 63-i = "parent i contains q", a 64x64 bit transpose per
@@ -528,6 +454,8 @@ size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm)
   });
   return r;
 }
+
+void gather_rows(Context& c, DList& l, const u32* perm) { compact_flags(c, l, nullptr, perm); }
 
 size_t compact_unique(Context& c, DList& l, const u32* perm) {
   size_t r = 0;

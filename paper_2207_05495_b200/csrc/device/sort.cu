@@ -171,8 +171,6 @@ size_t lex_sort_dedupe(Context& c, DList& l) {
   return before - compact_unique(c, l, perm);
 }
 
-__global__ void concat_kernel_dummy() {}
-
 void merge_sorted(Context& c, DList& h, const DList& add) {
   if (add.empty()) return;
   const size_t total = h.size() + add.size();

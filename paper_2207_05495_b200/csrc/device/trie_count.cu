@@ -35,7 +35,9 @@ template <int W>
 __global__ void __launch_bounds__(256) hist_kernel(const u64* __restrict__ words,
                                                    const u32* __restrict__ idx,
                                                    const u32* __restrict__ seg, u32 N, u32 n,
-                                                   u32* __restrict__ hist) {
+                                                   u32* __restrict__ hist,
+                                                   const u32* __restrict__ cards,
+                                                   u32* __restrict__ minc) {
   extern __shared__ u32 sh[];
   const u32 base = blockIdx.x * blockDim.x;
   const u32 i = base + threadIdx.x;
@@ -45,6 +47,12 @@ __global__ void __launch_bounds__(256) hist_kernel(const u64* __restrict__ words
   if (shared_mode) {
     for (u32 q = threadIdx.x; q < n; q += blockDim.x) sh[q] = 0;
     __syncthreads();
+  }
+  if (minc) {  // shape mode: per-segment min cardinality (warp-aggregated atomicMin)
+    const u32 s = i < N ? seg[i] : kInvalid;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, s);
+    const u32 m = __reduce_min_sync(peers, s != kInvalid ? cards[idx[i]] : 0xFFFFFFFFu);
+    if (s != kInvalid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minc[s], m);
   }
   if (i < N) {
     const u32 s = seg[i];
@@ -170,10 +178,17 @@ __global__ void init_kernel(u32* idx, u32* seg, u32 N) {
 
 }  // namespace
 
-u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
+// Builds the trie level by level; returns the node count and, with `shape`,
+// records every internal node (division state, min cardinality, internal
+// children) round by round.
+static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape) {
   const u64 N64 = l.size();
   if (N64 == 0) throw std::invalid_argument("StaticTrie: list must be non-empty");
   min_leaf = std::max<u32>(1, min_leaf);
+  if (shape) {
+    shape->rounds.clear();
+    shape->min_leaf = min_leaf;
+  }
   if (N64 <= min_leaf) return 1;
   const u32 N = static_cast<u32>(N64), n = c.n();
   cudaStream_t s = as_stream(c.stream());
@@ -186,7 +201,7 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
   Seg* segs = static_cast<Seg*>(c.alloc(max_segs * sizeof(Seg)));
   Seg* nsegs = static_cast<Seg*>(c.alloc(max_segs * sizeof(Seg)));
   // per-segment: div, zcount, child_zero, child_one, cursor_zero, cursor_one
-  u32* per = static_cast<u32*>(c.alloc(6ull * max_segs * 4));
+  u32* per = static_cast<u32*>(c.alloc(7ull * max_segs * 4));
   struct Ctr {
     u32 next_count;
     u32 pad;
@@ -209,6 +224,8 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
     }
     SW_CUDA(cudaMemsetAsync(hist, 0, hbytes, s));
     SW_CUDA(cudaMemsetAsync(per, 0, 6ull * max_segs * 4, s));
+    u32* minc = shape ? per + 6ull * max_segs : nullptr;
+    if (minc) SW_CUDA(cudaMemsetAsync(minc, 0xFF, static_cast<size_t>(nact) * 4, s));
     SW_CUDA(cudaMemsetAsync(&ctr->next_count, 0, 4, s));
     u32* div = per;
     u32* zc = per + max_segs;
@@ -217,7 +234,8 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
     u32* curz = per + 4ull * max_segs;
     u32* curo = per + 5ull * max_segs;
     SW_DISPATCH_W(c.W(), {
-      hist_kernel<W><<<(N + 255) / 256, 256, n * 4, s>>>(l.words, idx, seg, N, n, hist);
+      hist_kernel<W><<<(N + 255) / 256, 256, n * 4, s>>>(l.words, idx, seg, N, n, hist, l.cards,
+                                                         minc);
     });
     pick_kernel<<<(nact * 32 + 255) / 256, 256, 0, s>>>(hist, segs, nact, n, min_leaf, div, zc, cz,
                                                         co, nsegs, &ctr->next_count, &ctr->nodes);
@@ -227,6 +245,17 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
     });
     SW_CHECK_LAUNCH();
     c.counters.kernel_launches += 3;
+    if (shape) {
+      std::vector<u32> hd(4ull * nact), hm(nact);
+      c.memcpy_d2h(hd.data(), div, nact * 4ull);
+      c.memcpy_d2h(hd.data() + nact, cz, nact * 4ull);
+      c.memcpy_d2h(hd.data() + 2ull * nact, co, nact * 4ull);
+      c.memcpy_d2h(hm.data(), minc, nact * 4ull);
+      std::vector<TrieShape::Node> round(nact);
+      for (u32 i = 0; i < nact; ++i)
+        round[i] = TrieShape::Node{hd[i], hm[i], hd[nact + i], hd[2ull * nact + i]};
+      shape->rounds.push_back(std::move(round));
+    }
     std::swap(idx, idx2);
     std::swap(seg, seg2);
     std::swap(segs, nsegs);
@@ -245,6 +274,12 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) {
   SYNCHRO_PROGRESS("  trie node count over %llu sets: %llu nodes", static_cast<unsigned long long>(N64),
                    static_cast<unsigned long long>(h.nodes));
   return h.nodes;
+}
+
+u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) { return build_trie(c, l, min_leaf, nullptr); }
+
+u64 trie_shape(Context& c, const DList& l, u32 min_leaf, TrieShape* shape) {
+  return build_trie(c, l, min_leaf, shape);
 }
 
 }  // namespace synchro::dev

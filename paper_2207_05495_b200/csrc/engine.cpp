@@ -8,6 +8,7 @@
 #include <sstream>
 
 #include "device/dev.hpp"
+#include "meet_order.hpp"
 #include "progress.hpp"
 
 namespace synchro {
@@ -206,6 +207,9 @@ void GpuBibfs::bfs_step(bool with_history) {
   if (with_history) merge_history(*hbfs_, hbfs_i_, next);
   // commit (bibfs_engine.hpp:375-379)
   ledger_.release(list_footprint(n_, lbfs_i_.size));
+  if (lbfs_met_ && lbfs_i_.size >= opt_.tuning.min_brute)  // its meet permuted L_IBFS
+    met_lists_.push_back(std::make_unique<DList>(std::move(*lbfs_)));
+  lbfs_met_ = false;
   *lbfs_ = std::move(next);
   lbfs_index_.reset();
   refresh(*lbfs_, lbfs_i_);
@@ -262,6 +266,8 @@ void GpuBibfs::ibfs_step(bool with_history) {
   dev::complement(ctx_, next);
   ledger_.release(list_footprint(n_, libfs_i_.size));
   *libfs_ = std::move(next);
+  met_lists_.clear();  // a fresh L_IBFS in complement-lex order
+  lbfs_met_ = false;
   refresh(*libfs_, libfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
@@ -285,6 +291,7 @@ void GpuBibfs::perform(StepKind kind) {
 // Meet: is some X in L_BFS a subset of some Y in L_IBFS?
 // Small lists: one all-pairs launch instead of building the index.
 bool GpuBibfs::meet() {
+  lbfs_met_ = !opt_.track_word;  // meet_check permutes L_IBFS (subset_algebra.hpp:201-210)
   if (dev::brute_fits(lbfs_->size(), libfs_->size()))
     return dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, nullptr);
   return dev::exists_subset(ctx_, bfs_index(), *libfs_, nullptr);
@@ -301,8 +308,42 @@ bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
   return true;
 }
 
+void GpuBibfs::replay_meet_order() {
+  std::vector<const DList*> met;
+  for (const auto& l : met_lists_) met.push_back(l.get());
+  if (lbfs_met_ && lbfs_i_.size >= opt_.tuning.min_brute) met.push_back(lbfs_.get());
+  if (met.empty() || libfs_i_.size < 2) return;
+  const u32 W = ctx_.W();
+  std::vector<u64> B(libfs_i_.size * W);
+  dev::download(ctx_, *libfs_, B.data(), nullptr, nullptr);
+  std::vector<u32> order(libfs_i_.size);
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<u32>(i);
+  std::vector<u64> A;
+  for (const DList* l : met) {  // oldest first, as the meets ran
+    DList sorted = dev::copy_list(ctx_, *l, false);
+    dev::sort_lex(ctx_, sorted);  // L_BFS is lex-sorted unique in the reference
+    A.resize(sorted.size() * W);
+    dev::download(ctx_, sorted, A.data(), nullptr, nullptr);
+    replay_meet_check(A.data(), sorted.size(), B.data(), W, n_, opt_.tuning.min_brute, order);
+  }
+  u32* perm = static_cast<u32*>(ctx_.alloc(order.size() * 4));
+  ctx_.memcpy_h2d(perm, order.data(), order.size() * 4);
+  dev::gather_rows(ctx_, *libfs_, perm);
+  ctx_.free(perm);
+  met_lists_.clear();
+  lbfs_met_ = false;
+}
+
 // -------------------------------------------------------------- DFS phase
 namespace {
+
+// dfs_phase.hpp:74-80
+size_t dfs_slice_cap(const MemoryLedger& ledger, u32 n, u32 k, u64 bound, u64 r) {
+  const u64 set_bytes = words_for(n) * sizeof(u64);
+  const u64 levels = bound > r ? bound - r : 1;
+  const u64 denom = (k + 1) * levels * set_bytes;
+  return static_cast<size_t>(std::max<u64>(ledger.available() / std::max<u64>(denom, 1), 1));
+}
 
 // Analysis aid: with SYNCHRO_DUMP_DIR set, lists are written as raw u64 words.
 void dump_list(dev::Context& c, const DList& l, const std::string& name) {
@@ -364,12 +405,7 @@ class DfsRunner {
     ~Guard() { l.release(amount); }
   };
 
-  size_t slice_cap(u64 r) const {
-    const u64 set_bytes = words_for(c_.n()) * sizeof(u64);
-    const u64 levels = bound_ > r ? bound_ - r : 1;
-    const u64 denom = (c_.k() + 1) * levels * set_bytes;
-    return static_cast<size_t>(std::max<u64>(ledger_.available() / std::max<u64>(denom, 1), 1));
-  }
+  size_t slice_cap(u64 r) const { return dfs_slice_cap(ledger_, c_.n(), c_.k(), bound_, r); }
 
   void recurse(const DList& list, size_t lo, size_t hi, u64 r, u32 level, const Frame* parent) {
     deadline_.check();
@@ -415,12 +451,55 @@ class DfsRunner {
     }
     if (r >= bound_ - 1) return;
     const size_t cap = slice_cap(r);
-    if (next.size() > cap) dev::sort_card_desc_lex(c_, next);  // slices follow the order
+    if (next.size() > cap) {  // slices follow the order the trie queries left
+      dev::sort_card_desc_lex(c_, next);
+      replay_query_order(next, cap);
+    }
     const Frame frame{parent, &next};
     for (size_t plo = 0; plo < next.size(); plo += cap) {
       recurse(next, plo, std::min(next.size(), plo + cap), r + 1, level + 1, &frame);
       if (r >= bound_ - 1) return;
     }
+  }
+
+  // The reference queries the trie per cardinality group of the (card desc,
+  // lex)-sorted level, and each query permutes its group in place
+  // (static_trie.hpp:177-183) before the level is cut into slices of `cap`.
+  // Only groups that straddle a slice boundary change which sets share a
+  // slice; their order is replayed on the host (meet_order.cpp).
+  void replay_query_order(DList& level, size_t cap) {
+    const size_t N = level.size();
+    std::vector<u32> cards(N);
+    dev::download(c_, level, nullptr, cards.data(), nullptr);
+    std::vector<std::pair<size_t, size_t>> groups;
+    for (size_t b = cap; b < N; b += cap) {
+      if (cards[b - 1] != cards[b]) continue;  // boundary between two groups
+      size_t lo = b - 1, hi = b + 1;
+      while (lo > 0 && cards[lo - 1] == cards[b]) --lo;
+      while (hi < N && cards[hi] == cards[b]) ++hi;
+      if (groups.empty() || groups.back().first != lo) groups.emplace_back(lo, hi);
+    }
+    if (groups.empty()) return;
+    if (!shape_) {
+      shape_ = std::make_unique<dev::TrieShape>();
+      dev::trie_shape(c_, lbfs_, t_.min_leaf, shape_.get());
+    }
+    const u32 W = c_.W();
+    std::vector<u32> perm(N);
+    for (size_t i = 0; i < N; ++i) perm[i] = static_cast<u32>(i);
+    for (const auto& [lo, hi] : groups) {
+      DList g = dev::slice_copy(c_, level, lo, hi, false);
+      std::vector<u64> rows((hi - lo) * W);
+      dev::download(c_, g, rows.data(), nullptr, nullptr);
+      std::vector<u32> order(hi - lo);
+      for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<u32>(i);
+      replay_trie_query(*shape_, rows.data(), W, cards[lo], order);
+      for (size_t i = 0; i < order.size(); ++i) perm[lo + i] = static_cast<u32>(lo + order[i]);
+    }
+    u32* d = static_cast<u32*>(c_.alloc(N * 4));
+    c_.memcpy_h2d(d, perm.data(), N * 4);
+    dev::gather_rows(c_, level, d);
+    c_.free(d);
   }
 
   void record_find(const dev::Witness& w, const DList& level, const Frame* parent) {
@@ -451,6 +530,7 @@ class DfsRunner {
   size_t root_start_ = 0, root_stride_ = 1;
   DfsFind find_;
   std::set<u64> dumped_;
+  std::unique_ptr<dev::TrieShape> shape_;  // the reference trie over L_BFS, built on first use
 };
 
 }  // namespace
@@ -467,6 +547,10 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   const u64 trie_bytes = list_footprint(n_, lbfs_i_.size) + nodes * 24;
   ledger_.charge_or_throw(trie_bytes);
   ledger_.release(list_footprint(n_, lbfs_i_.size));
+  // The top-level slices follow L_IBFS's order: reproduce the reference's
+  // post-meet_check order when they will actually cut the list.
+  if (!opt_.track_word && r < R_ && libfs_i_.size > dfs_slice_cap(ledger_, n_, k_, R_, r - 1))
+    replay_meet_order();
   dump_list(ctx_, *lbfs_, "lbfs");
   dump_list(ctx_, *libfs_, "libfs");
   const dev::PermIndex& index = bfs_index();
@@ -599,6 +683,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
   };
 
   for (u64 r = 1; r + 1 <= R; ++r) {
+    if (opt.stop_after_iterations && res.iterations >= opt.stop_after_iterations)
+      return finish(0, std::nullopt, "stopped");
     eng.deadline().check();
     eng.set_iteration(r);
     eng.clear_failures();

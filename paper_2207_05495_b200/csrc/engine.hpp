@@ -53,11 +53,15 @@ struct SolveOptions {
   int device = -1;      // CUDA device (-1: current)
   bool timing = false;  // CUDA-event timing of the expansion kernels
   // Multi-GPU DFS partitioning (one process per GPU): this solve explores
-  // only the DFS subtrees rooted in its contiguous share of L_IBFS; the
-  // threshold of the whole search is the MIN over the shards.
+  // only the DFS subtrees rooted in its interleaved share of L_IBFS (rows
+  // i ≡ index mod count); the threshold of the whole search is the MIN over
+  // the shards.
   u32 dfs_shard_index = 0;
   u32 dfs_shard_count = 1;
   bool contain_stats = false;  // count traversal node visits / pair tests (analysis)
+  // Analysis / prefix-parity hook: stop before iteration stop_after_iterations+1
+  // (phase "stopped", threshold 0).  0 = run to the end.
+  u64 stop_after_iterations = 0;
 };
 
 struct SolveResult {
@@ -82,7 +86,7 @@ struct SolveResult {
   u64 contain_pairs = 0;         // range-scan pair tests (contain_stats)
   double engine_device_ms = 0;  // CUDA-event span of the engine on its stream
   u64 h2d_bytes = 0, d2h_bytes = 0;
-  std::string phase;            // meet | dfs | bound | trivial
+  std::string phase;            // meet | dfs | bound | trivial | stopped
   std::vector<std::array<u64, 5>> dfs_levels;  // r, level, in, generated, kept
 };
 
@@ -106,6 +110,9 @@ class GpuBibfs {
   void perform(StepKind kind);
   bool meet();
   bool meet_witness(size_t* bfs_index, u64* ibfs_tag);
+  // Reorders L_IBFS as the reference's in-place meet checks left it
+  // (meet_order.hpp); only needed when the DFS slices L_IBFS.
+  void replay_meet_order();
   u64 run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log, u64* expansions);
 
   void set_iteration(u64 r) { r_ = r; }
@@ -156,6 +163,10 @@ class GpuBibfs {
   std::array<bool, 4> failed_{false, false, false, false};
   u64 charged_layer_ = 0;
   std::vector<std::vector<u64>> bfs_levels_, ibfs_levels_;
+  // L_BFS lists met (meet_check, no tracking) since L_IBFS was last committed,
+  // oldest first; lbfs_met_: the current L_BFS has been met too.
+  std::vector<std::unique_ptr<dev::DList>> met_lists_;
+  bool lbfs_met_ = false;
 };
 
 void trace_line(std::ostream* trace, const GpuBibfs& eng, const SearchStats& s, const StepCosts& c,

@@ -2,8 +2,9 @@
 
 Every rank runs phase 1 (the list steps are deterministic, so all ranks hold
 identical L_BFS / L_IBFS and write identical trace prefixes), then explores
-only the DFS subtrees rooted in its contiguous share of L_IBFS
-(`dfs_shard_index/dfs_shard_count`, engine.cpp DfsRunner::run).  The DFS
+only the DFS subtrees rooted in its interleaved share of L_IBFS (rows
+i ≡ shard_index mod shard_count; `dfs_shard_index/dfs_shard_count`,
+engine.cpp DfsRunner::run).  The DFS
 returns the minimum depth at which any subtree meets L_BFS, so the threshold
 of the whole search is the MIN over ranks (one all-reduce); the word comes
 from the lowest rank attaining it.  Every reduction inside a DFS slice keeps a

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = [
     "sw_list_dedupe_sorted", "sw_list_hash_dedupe", "sw_list_self_reduce_minimal", "sw_list_mark",
     "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
     "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe", "sw_dev_owner_partition",
-    "sw_dev_hash_dedupe",
+    "sw_dev_hash_dedupe", "sw_solve_exact_ex", "sw_meet_check_order",
 ]
 
 
@@ -71,7 +71,10 @@ class SolveOptions(C.Structure):
         ("min_brute", C.c_uint32), ("min_leaf", C.c_uint32), ("dedupe_cadence", C.c_uint32),
         ("reduce_cadence", C.c_uint32), ("device", C.c_int32), ("timing", C.c_int32),
         ("dfs_shard_index", C.c_uint32), ("dfs_shard_count", C.c_uint32),
-        ("contain_stats", C.c_int32),
+        ("contain_stats", C.c_int32), ("dfs_largest", C.c_uint64),
+        ("history_growth", C.c_double), ("beam_initial", C.c_uint64),
+        ("beam_cost_fraction", C.c_double), ("reduction_of_reduction", C.c_double),
+        ("stop_after_iterations", C.c_uint64),
     ]
 
 
@@ -131,6 +134,11 @@ def load():
                                    C.POINTER(C.c_int32)]
     L.sw_solve_exact.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(SolveOptions),
                                  C.POINTER(SolveResultC), C.c_void_p, C.c_size_t, C.c_char_p]
+    L.sw_solve_exact_ex.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(SolveOptions),
+                                    C.POINTER(SolveResultC), C.c_void_p, C.c_size_t, C.c_char_p,
+                                    C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.sw_meet_check_order.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
+                                      C.c_uint32, _u32p]
     L.sw_heuristic.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_int32, C.c_uint64, C.c_uint64,
                                C.c_double, C.POINTER(C.c_uint64), C.c_void_p, C.c_size_t]
     L.sw_power_set_oracle.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_double,
@@ -319,6 +327,7 @@ class SolveResult:
     trace: Optional[List[str]] = field(default=None)
     contain_visits: int = 0
     contain_pairs: int = 0
+    dfs_levels: List[List[int]] = field(default_factory=list)  # [r, level, in, generated, kept]
 
     @property
     def expansions(self) -> int:
@@ -345,10 +354,15 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
     r = SolveResultC()
     cap = 1 << 20 if o.track_word else 0
     buf = np.zeros(max(cap, 1), np.uint32)
-    _check(load().sw_solve_exact(aut.n, aut.k, np.ascontiguousarray(aut.delta, np.uint32),
-                                 C.byref(o), C.byref(r), buf.ctypes.data_as(C.c_void_p), cap,
-                                 trace_path.encode() if trace_path else None))
+    lcap = 1 << 16
+    levels = np.zeros(5 * lcap, np.uint64)
+    nlev = C.c_size_t()
+    _check(load().sw_solve_exact_ex(aut.n, aut.k, np.ascontiguousarray(aut.delta, np.uint32),
+                                    C.byref(o), C.byref(r), buf.ctypes.data_as(C.c_void_p), cap,
+                                    trace_path.encode() if trace_path else None,
+                                    levels.ctypes.data_as(C.c_void_p), lcap, C.byref(nlev)))
     word = buf[: r.word_len].tolist() if r.has_word else None
+    dfs_levels = levels[: 5 * min(nlev.value, lcap)].reshape(-1, 5).tolist()
     trace = None
     if trace_path and os.path.exists(trace_path):
         with open(trace_path) as f:
@@ -358,7 +372,18 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
                        r.heuristic_seconds, r.engine_seconds, r.expand_kernel_ms,
                        r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
                        r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace,
-                       r.contain_visits, r.contain_pairs)
+                       r.contain_visits, r.contain_pairs, dfs_levels)
+
+
+def meet_check_order(n: int, a_words, b_words, min_brute: int = 64) -> np.ndarray:
+    """Host-side replay of the order the reference's meet_check leaves b in
+    (subset_algebra.hpp:201-210; no device).  order[p] = original index."""
+    W = (n + 63) // 64
+    a = np.ascontiguousarray(a_words, np.uint64)
+    b = np.ascontiguousarray(b_words, np.uint64)
+    out = np.zeros(b.size // W, np.uint32)
+    _check(load().sw_meet_check_order(n, a, a.size // W, b, b.size // W, min_brute, out))
+    return out
 
 
 ALGORITHMS = {"eppstein": 0, "beam": 1, "adaptive": 2}

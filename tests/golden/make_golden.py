@@ -72,6 +72,20 @@ SMALL = ["cerny:%d" % n for n in range(2, 13)] + ["cerny:20"] + \
         ["random:%d,%d,%d" % (n, k, s) for n in (20, 50, 100) for k in (2, 3) for s in range(3)]
 MEDIUM = ["random:200,2,1", "random:300,2,1", "random:100,3,0", "random:100,3,1"]
 LARGE = ["random:300,2,0", "random:300,2,2", "random:200,3,0"]
+# Budgets under which the DFS cuts its levels into slices (dfs_phase.hpp:52-56,
+# :153-158), with and without word tracking (meet_find copies L_IBFS, meet_check
+# permutes it: the top-level slices follow that order), plus non-default
+# EngineTuning / TuningParams fields (bibfs_engine.hpp:27-37, cost_model.hpp:26-36).
+SLICING = [("random:200,2,1", dict(upper_bound=37, memory=m, track_word=tw))
+           for m in (4 << 20, 8 << 20, 16 << 20) for tw in (0, 1)] + \
+          [("random:300,2,1", dict(upper_bound=39, memory=16 << 20, track_word=tw)) for tw in (0, 1)]
+TUNING = [("cerny:16", dict(history_growth=1.5)),
+          ("cerny:12", dict(history_growth=3.0)),
+          ("random:200,2,1", dict(dfs_largest=500)),
+          ("random:200,2,1", dict(dfs_largest=3000, memory=16 << 20)),
+          ("random:100,2,5", dict(reduction_of_reduction=0.3)),
+          ("random:150,2,4", dict(beam_initial=100, beam_cost_fraction=0.2)),
+          ("random:100,3,2", dict(beam_initial=16, beam_cost_fraction=0.01))]
 
 
 def main(which: str) -> None:
@@ -99,6 +113,17 @@ def main(which: str) -> None:
     if which in ("large", "all"):
         for s in LARGE:
             write("solve_" + s.replace(":", "_").replace(",", "_") + ".json", solve_case(s))
+    if which in ("slicing", "all"):
+        cases = []
+        for spec, opts in SLICING:
+            c = solve_case(spec, **opts)
+            depths = {}
+            for lv in c["dfs_levels"]:
+                depths[lv["r"]] = depths.get(lv["r"], 0) + 1
+            assert max(depths.values()) > 1, (spec, opts)  # the DFS really slices
+            cases.append(c)
+        cases += [solve_case(spec, **opts) for spec, opts in TUNING]
+        write("solve_slicing.json", cases)
     if which in ("batch", "all"):
         # config 2: 1000 random binary automata n=100, instance_seed(0, 100, i)
         rows = []

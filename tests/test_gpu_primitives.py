@@ -275,3 +275,43 @@ dist.destroy_process_group()
     out = np.load(tmp_path / "o.npy")
     assert sorted(rows(n, out)) == sorted(set(rows(n, words)))
     assert "sent 0" in p.stdout
+
+
+_OVERFLOW_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+from helpers import W, lex_sorted_unique, random_list
+from paper_2207_05495_b200 import native as gpu
+from oracle import ref
+bad = []
+for n, da, db in [(300, 0.05, 0.2), (100, 0.05, 0.3), (570, 0.03, 0.2)]:
+    a = lex_sorted_unique(n, random_list(n, 30000, da, 1))
+    b = np.concatenate([random_list(n, 8000, db, 2), a[: 100 * W(n)]])
+    for mode in (0, 1):
+        if not np.array_equal(gpu.list_mark(n, a, b, mode), ref.mark(n, a, b, mode)):
+            bad.append(("mark", n, mode))
+    if gpu.list_self_reduce_minimal(n, a).tobytes() != ref.self_reduce_minimal(n, a).tobytes():
+        bad.append(("self", n))
+    if gpu.list_meet_check(n, a, b[: 2000 * W(n)]) != ref.meet_check(n, a, b[: 2000 * W(n)]):
+        bad.append(("meet", n))
+print("BAD", bad)
+"""
+
+
+@pytest.mark.parametrize("spill_cap", ["0", "128"])
+def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap):
+    """contain.cu: when a warp's task pool and its spill stack are both full, the
+    opened range is scanned instead of descended.  SYNCHRO_SPILL_CAP shrinks the
+    stack so that path runs (the progress log counts overflow scans); marks,
+    self-reduction and meet must still equal the reference's
+    (subset_algebra.hpp:55-231)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SYNCHRO_SPILL_CAP=spill_cap, SYNCHRO_PROGRESS="1")
+    p = subprocess.run([sys.executable, "-c", _OVERFLOW_PROBE, root], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "BAD []" in p.stdout, p.stdout
+    scans = [int(x) for x in __import__("re").findall(r"overflow_scans=(\d+)", p.stderr)]
+    assert scans and max(scans) > 0, "overflow path not exercised"
