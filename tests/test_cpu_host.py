@@ -229,3 +229,22 @@ def test_reference_small_solve_reproduces_golden(ref, tmp_path):
         a = sw.from_spec(c["spec"])
         s = ref.solve_exact(a.n, a.k, a.delta, trace_path=str(tmp_path / "t"), **c["options"])
         assert s.threshold == c["threshold"] and s.trace == c["trace"]
+
+
+def test_reference_side_shim_compiles_against_reference_headers(tmp_path):
+    """include/synchro_b200_shim.hpp (the binding a maintainer of the reference
+    adds) compiles against the unmodified reference headers
+    and links the product library; the driver runs host-only entry points."""
+    inc = "/root/reference/proj/include"
+    if not os.path.isdir(inc):
+        pytest.skip("reference headers not present")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "shim_driver"
+    libdir = os.path.join(root, "paper_2207_05495_b200", "lib")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", f"-I{inc}", f"-I{root}/include",
+                        os.path.join(root, "oracle", "shim_driver.cpp"), "-o", str(exe),
+                        f"-L{libdir}", "-lsynchro_b200", f"-Wl,-rpath,{libdir}", "-pthread"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    v = subprocess.run([str(exe), "--version"], capture_output=True, text=True, timeout=60)
+    assert v.returncode == 0 and "dfs_largest=20000 history_growth=2" in v.stdout

@@ -88,3 +88,38 @@ def test_engine_step_api_replays_golden_schedule(gpu):
     assert eng.choose(r_dfs) == "DFS"
     assert eng.dfs(r_dfs) == case["threshold"]
     eng.close()
+
+
+SHIM = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                    "shim_driver")
+# spec memory track_word upper_bound dfs_largest history_growth beam_initial
+# beam_cost_fraction reduction_of_reduction set_cost
+SHIM_CASES = [
+    "cerny:16 4294967296 1 0 20000 1.5 0 0.05 0 512",
+    "cerny:12 4294967296 0 0 20000 3.0 0 0.05 0 512",
+    "random:200,2,1 4294967296 0 0 500 2.0 0 0.05 0 512",
+    "random:200,2,1 16777216 1 0 3000 2.0 0 0.05 0 512",
+    "random:200,2,1 4194304 0 37 20000 2.0 0 0.05 0 512",
+    "random:100,2,5 4294967296 0 0 20000 2.0 0 0.05 0.3 512",
+    "random:150,2,4 4294967296 1 0 20000 2.0 100 0.2 0 256",
+    "random:100,3,2 4294967296 0 0 20000 2.0 16 0.01 0 512",
+]
+
+
+@pytest.mark.skipif(not os.path.exists(SHIM), reason="shim driver not built (needs the reference)")
+def test_reference_side_shim_matches_reference_solve(gpu):
+    """include/synchro_b200_shim.hpp compiled against the unmodified reference
+    headers (oracle/Makefile `shim`): synchro::solve_exact_b200 with every
+    EngineTuning / TuningParams field forwarded returns the reference's
+    SolveResult (bibfs_engine.hpp:50-59) and the same trace as the reference's
+    own synchro::solve_exact, on non-default dfs_largest, history_growth,
+    beam_initial, beam_cost_fraction, reduction_of_reduction and set_cost."""
+    r = subprocess.run([SHIM], input="\n".join(SHIM_CASES) + "\n", capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert len(lines) == len(SHIM_CASES)
+    for line in lines:
+        spec, ref_part, b200_part, flags = [x.strip() for x in line.split("|")]
+        assert ref_part[4:] == b200_part[5:], line
+        assert flags == "1 1", line
