@@ -297,7 +297,10 @@ constexpr int kPoolThreads = kPoolWarps * 32;
 // bottom half (the oldest tasks) is spilled to a per-warp stack in global
 // memory and pulled back before new queries are taken; only when that stack
 // is full too does the opened range fall back to a scan.
-constexpr int kPoolCap = 256;
+#ifndef SW_POOL_CAP
+#define SW_POOL_CAP 256
+#endif
+constexpr int kPoolCap = SW_POOL_CAP;
 constexpr int kSpill = kPoolCap / 2;
 constexpr int kSpillCap = 1024;  // tasks per warp in the global spill stack
 constexpr int kPoolBrute = kScanKeys;  // ranges of <= this many keys are scanned

@@ -248,3 +248,21 @@ def test_reference_side_shim_compiles_against_reference_headers(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     v = subprocess.run([str(exe), "--version"], capture_output=True, text=True, timeout=60)
     assert v.returncode == 0 and "dfs_largest=20000 history_growth=2" in v.stdout
+
+
+def test_slow_sync_series_fixture_text_and_oracle():
+    """Config 5 series fixture (tests/golden/make_config5.py): every automaton
+    parses from its text form (automaton.hpp:178-219) and the host power-set
+    BFS oracle reproduces the reference-pinned threshold."""
+    cases = json.load(open(os.path.join(GOLDEN, "slow_sync_series.json")))
+    assert len(cases) >= 40
+    names = {c["name"] for c in cases}
+    assert {"wielandt:20", "cerny:19", "ternary5_roman", "climb:10"} <= names
+    for c in cases:
+        aut = sw.parse_automaton(c["text"])
+        assert (aut.n, aut.k) == (c["n"], c["k"])
+        if c["n"] <= 16:
+            assert sw.power_set_oracle(aut) == c["oracle"] == c["threshold"], c["name"]
+    w = {c["name"]: c["threshold"] for c in cases}
+    for n in range(3, 21):  # Wielandt series: n^2 - 3n + 3
+        assert w[f"wielandt:{n}"] == n * n - 3 * n + 3
