@@ -141,6 +141,49 @@ int sw_solve_exact_ex(uint32_t n, uint32_t k, const uint32_t* delta, const sw_so
                       const char* trace_path, uint64_t* dfs_levels, size_t dfs_levels_cap,
                       size_t* dfs_levels_count);
 
+/* ---- partitioned solve over several GPUs (no reference
+ * counterpart: the reference solves on one thread).  One process per GPU;
+ * every rank calls sw_solve_exact_dist with the same automaton and options.
+ * Subsets are owned by hash (owner = h(set) mod nranks); each level, one
+ * all-to-all carries generated subsets to their owners, which deduplicate;
+ * containment (self-reduction, history, meet) all-gathers what it needs;
+ * the cost model's statistics are all-reduced, so every rank takes the
+ * reference's step sequence and prints the same trace; the DFS runs one
+ * interleaved share of L_IBFS per rank and the threshold is the MIN.
+ * Transport: NCCL on device buffers (nccl_id from sw_nccl_unique_id on one
+ * rank, shared by the caller), or host-buffer callbacks (any transport).
+ * Callbacks return 0 on success; buffers are host memory:
+ *   all_to_allv: send holds send_bytes[r] bytes for rank r, rank by rank;
+ *                recv receives recv_bytes[r] bytes from rank r, rank by rank;
+ *   all_gather_v: every rank contributes `bytes`; recv holds recv_bytes[r]
+ *                from rank r, rank by rank;
+ *   all_reduce_u64: in place, op 0 sum, 1 min, 2 max. ---- */
+#define SW_COMM_NCCL 1
+#define SW_COMM_CALLBACK 2
+typedef struct sw_comm {
+  int32_t kind;     /* SW_COMM_NCCL | SW_COMM_CALLBACK */
+  int32_t rank;
+  int32_t nranks;
+  int32_t pad;
+  uint8_t nccl_id[128];
+  void* user;
+  int (*all_to_allv)(void* user, const void* send, const uint64_t* send_bytes, void* recv,
+                     const uint64_t* recv_bytes);
+  int (*all_gather_v)(void* user, const void* send, uint64_t bytes, void* recv,
+                      const uint64_t* recv_bytes);
+  int (*all_reduce_u64)(void* user, uint64_t* values, uint64_t count, int32_t op);
+} sw_comm;
+typedef struct sw_comm_handle sw_comm_handle;
+int sw_nccl_unique_id(uint8_t* out128);
+/* Creates the transport (NCCL: ncclCommInitRank, collective over the ranks). */
+int sw_comm_create(const sw_comm* desc, sw_comm_handle** out);
+int sw_comm_destroy(sw_comm_handle* h);
+/* As sw_solve_exact_ex; result counters are global (all ranks); the word is
+ * returned by every rank (reconstructed from all-gathered level tags). */
+int sw_solve_exact_dist(uint32_t n, uint32_t k, const uint32_t* delta, const sw_solve_options* opt,
+                        sw_comm_handle* comm, sw_solve_result* result, uint32_t* word,
+                        size_t word_cap, const char* trace_path, uint64_t* nvlink_bytes);
+
 /* ---- heuristics (heuristics.hpp:26-184) ----
  * algorithm: 0 eppstein, 1 beam, 2 adaptive.  Returns SW_ERR_REFUSED when the
  * beam finds no reset word (CLI exit 5). */
@@ -212,6 +255,11 @@ int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count, const uint
                  size_t b_count, int32_t mode, uint8_t* keep);
 int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_count,
                        const uint64_t* b_words, size_t b_count, int32_t* met);
+/* Is some a element a subset of some b element, through the trie index
+ * (device/trie_query.cu; a in any order, duplicate-free)?  Witness positions. */
+int sw_list_trie_exists(uint32_t n, const uint64_t* a_words, size_t a_count,
+                        const uint64_t* b_words, size_t b_count, int32_t* met,
+                        uint64_t* a_index, uint64_t* b_index);
 /* Host-side (no device): the order in which the reference's meet_check
  * (subset_algebra.hpp:201-210) leaves b when it finds no containment:
  * order[p] = original index of the element now at position p.  a must be

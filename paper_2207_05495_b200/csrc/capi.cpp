@@ -10,6 +10,7 @@
 #include <string>
 
 #include "device/dev.hpp"
+#include "comm.hpp"
 #include "engine.hpp"
 #include "experiment.hpp"
 #include "meet_order.hpp"
@@ -21,6 +22,7 @@ using namespace synchro;
 namespace {
 
 thread_local std::string g_last_error;
+thread_local synchro::Comm* t_comm = nullptr;  // the communicator of sw_solve_exact_dist
 
 template <class F>
 int guarded(F&& f) {
@@ -204,6 +206,7 @@ SW_EXPORT int sw_solve_exact_ex(uint32_t n, uint32_t k, const uint32_t* delta,
     std::memset(out, 0, sizeof(*out));
     const Automaton aut = make_aut(n, k, delta);
     SolveOptions opt = to_options(o);
+    opt.comm = t_comm;
     std::ofstream trace;
     if (trace_path && *trace_path) {
       trace.open(trace_path);
@@ -241,6 +244,46 @@ SW_EXPORT int sw_solve_exact_ex(uint32_t n, uint32_t k, const uint32_t* delta,
       for (size_t i = 0; i < r.dfs_levels.size() && i < dfs_levels_cap; ++i)
         for (int f = 0; f < 5; ++f) dfs_levels[5 * i + f] = r.dfs_levels[i][f];
   });
+}
+
+struct sw_comm_handle {
+  std::unique_ptr<Comm> comm;
+};
+
+SW_EXPORT int sw_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] { nccl_unique_id(out128); });
+}
+
+SW_EXPORT int sw_comm_create(const sw_comm* desc, sw_comm_handle** out) {
+  return guarded([&] {
+    if (!desc || !out) throw std::invalid_argument("sw_comm_create: NULL argument");
+    auto h = std::make_unique<sw_comm_handle>();
+    h->comm = make_comm(*desc);
+    *out = h.release();
+  });
+}
+
+SW_EXPORT int sw_comm_destroy(sw_comm_handle* h) {
+  return guarded([&] { delete h; });
+}
+
+SW_EXPORT int sw_solve_exact_dist(uint32_t n, uint32_t k, const uint32_t* delta,
+                                  const sw_solve_options* o, sw_comm_handle* comm,
+                                  sw_solve_result* out, uint32_t* word, size_t word_cap,
+                                  const char* trace_path, uint64_t* nvlink_bytes) {
+  if (!comm) {
+    g_last_error = "sw_solve_exact_dist: no communicator";
+    return SW_ERR_PARSE;
+  }
+  sw_solve_options opt;
+  if (o) opt = *o; else sw_default_options(&opt);
+  const u64 before = comm->comm->bytes_sent;
+  t_comm = comm->comm.get();
+  const int rc = sw_solve_exact_ex(n, k, delta, &opt, out, word, word_cap, trace_path, nullptr, 0,
+                                   nullptr);
+  t_comm = nullptr;
+  if (nvlink_bytes) *nvlink_bytes = comm->comm->bytes_sent - before;
+  return rc;
 }
 
 SW_EXPORT int sw_heuristic(uint32_t n, uint32_t k, const uint32_t* delta, int32_t algorithm,
@@ -484,6 +527,14 @@ SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
       c.free(dkeep);
       return;
     }
+    if (dev::use_trie_index()) {
+      const dev::TrieQueryIndex t = dev::build_trie_index(c, a, dev::kTrieLeafKeys);
+      uint8_t* dkeep = static_cast<uint8_t*>(c.alloc(std::max<size_t>(b_count, 1)));
+      dev::trie_superset_flags(c, t, b, mode == 1, dkeep);
+      c.memcpy_d2h(keep, dkeep, b_count);
+      c.free(dkeep);
+      return;
+    }
     const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
     const std::vector<uint8_t> k = dev::superset_keep(c, ix, b, mode == 1);
     std::memcpy(keep, k.data(), k.size());
@@ -500,8 +551,28 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
     dev::Context c(identity_aut(n));
     dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    if (dev::use_trie_index()) {
+      const dev::TrieQueryIndex t = dev::build_trie_index(c, a, dev::kTrieLeafKeys);
+      *met = dev::trie_exists_subset(c, t, b, nullptr) ? 1 : 0;
+      return;
+    }
     const dev::PermIndex ix = dev::build_perm_index(c, a, dev::StateOrder::FreqDesc);
     *met = dev::exists_subset(c, ix, b, nullptr) ? 1 : 0;
+  });
+}
+
+SW_EXPORT int sw_list_trie_exists(uint32_t n, const uint64_t* a_words, size_t a_count,
+                                  const uint64_t* b_words, size_t b_count, int32_t* met,
+                                  uint64_t* a_index, uint64_t* b_index) {
+  return guarded([&] {
+    dev::Context c(identity_aut(n));
+    dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
+    dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    const dev::TrieQueryIndex t = dev::build_trie_index(c, a, dev::kTrieLeafKeys);
+    dev::Witness w;
+    *met = dev::trie_exists_subset(c, t, b, &w) ? 1 : 0;
+    if (a_index) *a_index = *met ? w.a_index : 0;
+    if (b_index) *b_index = *met ? w.b_index : 0;
   });
 }
 

@@ -122,11 +122,30 @@ __global__ void karras_kernel(const u64* __restrict__ A, u32 N, Node* __restrict
   else parent_int[gamma + 1] = static_cast<u32>(i);
 }
 
+// Filter words of a set: its relabelled word 0 (the index's first 64 states
+// in its state order) and its OR-fold (state q -> bit q mod 64).  Both are
+// monotone, so x ⊆ y implies sig(x) ⊆ sig(y) word by word: a one-word test
+// per pair rejects almost every non-containment (the fold for sparse sets, word
+// 0 for dense queries against a FreqDesc index), and only survivors are
+// checked on their full rows.
+template <int W>
+__device__ __forceinline__ ulonglong2 filter_words(const u64 (&x)[W]) {
+  u64 f = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) f |= x[w];
+  return make_ulonglong2(x[0], f);
+}
+__device__ __forceinline__ bool filter_pass(ulonglong2 x, ulonglong2 y) {
+  return ((x.x & ~y.x) | (x.y & ~y.y)) == 0;
+}
+
 // Bottom-up min cardinality: the second child to arrive at a node finishes it.
 // Nodes small enough to be scanned (<= small keys) also get the AND of their
 // keys: a query lacking one of those states cannot contain any of them, so the
 // scan is skipped (measured at n=300: 49% of meet/DFS scans, 61% of
-// self-reduction scans).
+// self-reduction scans).  The AND mask is reduced to its filter words, kept in
+// the node itself (window, pad: a scanned node never uses its prefix window),
+// so the skip needs no load beyond the node.
 template <int W>
 __global__ void mincard_kernel(const u32* __restrict__ card, const u64* __restrict__ keys, u32 N,
                                Node* nodes, const u32* __restrict__ parent_int,
@@ -154,6 +173,12 @@ __global__ void mincard_kernel(const u32* __restrict__ card, const u64* __restri
                                         : va[static_cast<u64>(split + 1) * W + w];
         va[static_cast<u64>(p) * W + w] = l & r;
       }
+      u64 m[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) m[w] = va[static_cast<u64>(p) * W + w];
+      const ulonglong2 f = filter_words<W>(m);
+      vn[p].window = f.x;
+      vn[p].pad = f.y;
     }
     if (p == 0) return;
     p = parent_int[p];
@@ -175,14 +200,14 @@ ContainIndex build_index(Context& c, const DList& a) {
   u32* arr = static_cast<u32*>(c.alloc(static_cast<size_t>(N) * 4));
   SW_CUDA(cudaMemsetAsync(arr, 0, static_cast<size_t>(N) * 4, s));
   SW_DISPATCH_W(c.W(), { karras_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(a.words, N, nodes, pint, pleaf); });
-  ix.andmask = c.alloc(static_cast<size_t>(N - 1) * c.W() * 8);
+  u64* andm = static_cast<u64*>(c.alloc(static_cast<size_t>(N - 1) * c.W() * 8));  // build only
   SW_DISPATCH_W(c.W(), {
     mincard_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(a.cards, a.words, N, nodes, pint, pleaf,
-                                                       arr, static_cast<u64*>(ix.andmask),
-                                                       kScanKeys);
+                                                       arr, andm, kScanKeys);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 2;
+  c.free(andm);
   c.free(pint);
   c.free(pleaf);
   c.free(arr);
@@ -229,7 +254,7 @@ __device__ __forceinline__ bool is_subset(const u64 (&x)[W], const u64 (&y)[W]) 
 template <int W, bool PAD>
 __global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
                                u32 n, const uint16_t* __restrict__ g_pos, u64* __restrict__ dst,
-                               u32* __restrict__ dcard) {
+                               u32* __restrict__ dcard, ulonglong2* __restrict__ dsig) {
   extern __shared__ uint16_t s_pos[];
   for (u32 q = threadIdx.x; q < n; q += blockDim.x) s_pos[q] = g_pos[q];
   __syncthreads();
@@ -254,6 +279,7 @@ __global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restric
       constexpr int P = Row<W>::P;
 #pragma unroll
       for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? acc[w] : (w == W ? scard[i] : 0);
+      dsig[i] = filter_words<W>(acc);
     } else {
 #pragma unroll
       for (int w = 0; w < W; ++w) dst[i * W + w] = acc[w];
@@ -265,12 +291,16 @@ __global__ void relabel_kernel(const u64* __restrict__ src, const u32* __restric
 // Plain sorted rows -> padded rows.
 template <int W>
 __global__ void pad_kernel(const u64* __restrict__ src, const u32* __restrict__ scard, u64 count,
-                           u64* __restrict__ dst) {
+                           u64* __restrict__ dst, ulonglong2* __restrict__ dsig) {
   constexpr int P = Row<W>::P;
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u64 x[W];
 #pragma unroll
-    for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? src[i * W + w] : (w == W ? scard[i] : 0);
+    for (int w = 0; w < W; ++w) x[w] = src[i * W + w];
+#pragma unroll
+    for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? x[w] : (w == W ? scard[i] : 0);
+    dsig[i] = filter_words<W>(x);
   }
 }
 
@@ -307,11 +337,24 @@ constexpr int kPoolBrute = kScanKeys;  // ranges of <= this many keys are scanne
 constexpr int kHitSlots = 32;
 constexpr u32 kNone = 0xFFFFFFFFu;
 
+#ifndef SW_POOL_MINB_WIDE
+#define SW_POOL_MINB_WIDE 1
+#endif
+#ifndef SW_POOL_MINB_NARROW
+#define SW_POOL_MINB_NARROW 6
+#endif
+// Resident CTAs per SM: 6 for W <= 6 (56 registers); wider rows need more
+// registers per lane (the query row, the key row of a leaf).
+constexpr int pool_min_blocks(int W) {
+  return W <= 6 ? SW_POOL_MINB_NARROW : (W <= 10 ? SW_POOL_MINB_WIDE : 1);
+}
+
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_kernel(
-    const u64* __restrict__ A, const Node* __restrict__ nodes, u32 Na, const u64* __restrict__ B,
-    u32 Nb, uint8_t* keep, int* found, unsigned long long* wit, u32* next_query, uint4* spill_all,
-    u32* overflow_scans, unsigned long long* stats, const u64* __restrict__ andm, u32 spill_cap) {
+__global__ void __launch_bounds__(kPoolThreads, pool_min_blocks(W)) contain_pool_kernel(
+    const u64* __restrict__ A, const ulonglong2* __restrict__ Asig, const Node* __restrict__ nodes,
+    u32 Na, const u64* __restrict__ B, const ulonglong2* __restrict__ Bsig, u32 Nb, uint8_t* keep,
+    int* found, unsigned long long* wit, u32* next_query, uint4* spill_all, u32* overflow_scans,
+    unsigned long long* stats, u32 spill_cap) {
   __shared__ u32 s_q[kPoolWarps][kPoolCap];
   __shared__ u32 s_n[kPoolWarps][kPoolCap];
   __shared__ u32 s_f[kPoolWarps][kPoolCap];
@@ -334,6 +377,18 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
   // its L2 round trip overlaps a round of work (a blocking check at the top of
   // every round was 25% of the stall samples on the DFS queries).
   int found_seen = 0;
+  // A confirmed containment: MARK drops the query, EXIST records the witness.
+  auto report = [&](u32 key, u32 q) {
+    if (EXIST) {
+      if (atomicCAS(found, 0, 1) == 0) {
+        wit[0] = key;
+        wit[1] = q;
+      }
+    } else {
+      keep[q] = 0;
+      shit[q % kHitSlots] = q;
+    }
+  };
   while (true) {
     if (EXIST) {
       if (found_seen) break;
@@ -394,22 +449,23 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
     const u32 limit = PROPER ? cy - 1 : cy;
     const bool is_leaf = (id & kLeafBit) != 0;
 
-    // ---- one concurrent round of loads.  A leaf needs its key row and the
-    // whole query row; an internal node only the node and the query's words
-    // d/64 and d/64+1: with need = lcp - d <= 64 the unchecked prefix bits
-    // [d, lcp) and the split bit lcp all lie in them (bits below d are
-    // masked).  Brute ranges and longer runs fetch the whole row in round 2.
+    // ---- one concurrent round of loads: the query's filter words, and the
+    // node (internal: + the query's words d/64 and d/64+1 — with need = lcp - d
+    // <= 64 the unchecked prefix bits [d, lcp) and the split bit lcp all lie in
+    // them; bits below d are masked) or the leaf key's filter words.  Full rows
+    // are fetched only for long runs and for pairs that pass the filter.
     u64 y[W], xf[W];
     u32 ycard = 0, kcard = 0;
     u64 ya = 0, yb = 0;
+    ulonglong2 qs = make_ulonglong2(0, 0), ks = make_ulonglong2(0, 0);
     const int q0 = d >> 6;
     Node nd{};
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = xf[w] = 0;
     if (have) {
+      qs = __ldg(Bsig + j);
       if (is_leaf) {
-        load_row<W>(B, j, y, ycard);
-        load_row<W>(A, first, xf, kcard);
+        ks = __ldg(Asig + first);
       } else {
         nd = load_node(nodes + id);
         const u64* yr = B + static_cast<u64>(j) * Row<W>::P;
@@ -420,18 +476,17 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
     auto yword = [&](int q) { return q == q0 ? ya : (q == q0 + 1 ? yb : u64{0}); };
 
     // ---- evaluate the task
-    bool hit = false, brute = false, longrun = false;
+    bool hit = false, brute = false, longrun = false, leafcheck = false;
     u32 hit_a = 0, c0 = kNone, c1 = kNone, f0 = 0, f1 = 0, bf = 0, bl = 0;
     int dchild = 0, L = 0;
     if (have) {
       if (is_leaf) {
-        if (kcard <= limit && is_subset<W>(xf, y)) {
-          hit = true;
-          hit_a = first;
-        }
+        leafcheck = filter_pass(ks, qs);
       } else if (nd.minc <= limit) {
         if (nd.last - nd.first < kPoolBrute) {
-          brute = true;
+          // every key of the range holds the node's AND states: skip the scan
+          // unless their filter words lie in the query's
+          brute = filter_pass(make_ulonglong2(nd.window, nd.pad), qs);
           bf = nd.first;
           bl = nd.last;
         } else {
@@ -461,18 +516,16 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
         }
       }
     }
-    // ---- round 2: whole query rows for brute ranges (their owner's row is
-    // shuffled to the scanning lanes) and long common runs
-    if (brute || longrun) load_row<W>(B, j, y, ycard);
-    if (brute) {  // every key of the range holds the node's AND states: all must be in y
-      u64 bad = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) bad |= __ldg(andm + static_cast<u64>(id) * W + w) & ~y[w];
-      if (bad) brute = false;
+    // ---- round 2: whole rows for long common runs and leaves that passed the filter
+    if (longrun || leafcheck) {
+      load_row<W>(B, j, y, ycard);
+      load_row<W>(A, longrun ? nd.first : first, xf, kcard);
+    }
+    if (leafcheck && kcard <= limit && is_subset<W>(xf, y)) {
+      hit = true;
+      hit_a = first;
     }
     if (longrun) {
-      u32 kc;
-      load_row<W>(A, nd.first, xf, kc);
       u64 bad = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) bad |= xf[w] & ~y[w] & range_mask(w, d, L);
@@ -532,13 +585,9 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
       sp -= kSpill;
     }
     if (sp + n0 + n1 > kPoolCap) {
-      // Pool and spill stack full: scan the opened range instead of descending.
-      // An internal-node task loaded only query words d/64, d/64+1 (a long run
-      // loaded the whole row): the scan needs all of y.
-      if (c0 != kNone) {
-        if (!longrun) load_row<W>(B, j, y, ycard);
-        brute = true;
-      }
+      // Pool and spill stack full: scan the opened range instead of descending
+      // (the scan needs only the query's filter words, already loaded).
+      if (c0 != kNone) brute = true;
       if (lane == 0) atomicAdd(overflow_scans, 1u);
     } else {
       if (c1 != kNone) {
@@ -559,7 +608,9 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
     }
     __syncwarp();
 
-    // ---- cooperative scan of small ranges: (range, key) pairs flattened over lanes
+    // ---- cooperative scan of small ranges: (range, key) pairs flattened over
+    // lanes; each pair first compares filter words (16 B per key), and only a
+    // pair that passes loads both full rows for the exact test.
     const u32 cnt = brute ? bl - bf + 1 : 0;
     u32 incl = cnt;
 #pragma unroll
@@ -583,38 +634,21 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
       const u32 o_bf = __shfl_sync(FULL, bf, owner);
       const u32 o_j = __shfl_sync(FULL, j, owner);
       const u32 o_lim = __shfl_sync(FULL, limit, owner);
-      u64 oy[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) oy[w] = __shfl_sync(FULL, y[w], owner);
+      const ulonglong2 oq = make_ulonglong2(__shfl_sync(FULL, qs.x, owner),
+                                            __shfl_sync(FULL, qs.y, owner));
       if (t < total) {
         const u32 key = o_bf + (t - o_excl);
-        u64 kr[W];
-        u32 kc = 0;
-        load_row<W>(A, key, kr, kc);
-        if (kc <= o_lim && is_subset<W>(kr, oy)) {
-          if (EXIST) {
-            if (atomicCAS(found, 0, 1) == 0) {
-              wit[0] = key;
-              wit[1] = o_j;
-            }
-          } else {
-            keep[o_j] = 0;
-            shit[o_j % kHitSlots] = o_j;
-          }
+        if (filter_pass(__ldg(Asig + key), oq)) {  // rare: the exact test, word by word
+          const u64* kr = A + static_cast<u64>(key) * Row<W>::P;
+          const u64* yr = B + static_cast<u64>(o_j) * Row<W>::P;
+          u64 acc = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc |= __ldg(kr + w) & ~__ldg(yr + w);
+          if (static_cast<u32>(__ldg(kr + W)) <= o_lim && acc == 0) report(key, o_j);
         }
       }
     }
-    if (hit) {
-      if (EXIST) {
-        if (atomicCAS(found, 0, 1) == 0) {
-          wit[0] = hit_a;
-          wit[1] = j;
-        }
-      } else {
-        keep[j] = 0;
-        shit[j % kHitSlots] = j;
-      }
-    }
+    if (hit) report(hit_a, j);
     __syncwarp();
   }
 }
@@ -622,8 +656,8 @@ __global__ void __launch_bounds__(kPoolThreads, (W <= 6 ? 6 : 1)) contain_pool_k
 // keep[j] = !hit (MARK) or *found/wit (EXIST) for padded queries Bp against
 // the padded keys of index p.
 template <bool PROPER, bool EXIST>
-static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, uint8_t* keep,
-                         int* found, unsigned long long* wit) {
+static void launch_query(Context& c, const PermIndex& p, const u64* Bp, const void* Bsig, u64 Nb,
+                         uint8_t* keep, int* found, unsigned long long* wit) {
   if (!Nb) return;
   cudaStream_t s = as_stream(c.stream());
   if (!EXIST) SW_CUDA(cudaMemsetAsync(keep, 1, Nb, s));
@@ -674,9 +708,10 @@ static void launch_query(Context& c, const PermIndex& p, const u64* Bp, u64 Nb, 
   }
   SW_DISPATCH_W(c.W(), {
     contain_pool_kernel<W, PROPER, EXIST><<<grid, kPoolThreads, 0, s>>>(
-        p.keys, static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
-        static_cast<u32>(Nb), keep, found, wit, counter, spill, counter + 1, stats,
-        static_cast<const u64*>(p.tree.andmask), spill_cap);
+        p.keys, static_cast<const ulonglong2*>(p.tree.keysig),
+        static_cast<const Node*>(p.tree.nodes), static_cast<u32>(p.count), Bp,
+        static_cast<const ulonglong2*>(Bsig), static_cast<u32>(Nb), keep, found, wit, counter,
+        spill, counter + 1, stats, spill_cap);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
@@ -741,14 +776,15 @@ PermIndex& PermIndex::operator=(PermIndex&& o) noexcept {
   return *this;
 }
 
-// Relabelled copy of l: padded rows (queries) or a plain list.
-static u64* relabel_padded(Context& c, const DList& l, const uint16_t* pos) {
+// Relabelled copy of l as padded query rows, plus their filter words.
+static u64* relabel_padded(Context& c, const DList& l, const uint16_t* pos, void** sig) {
   u64* out = nullptr;
+  *sig = c.alloc(std::max<size_t>(l.size(), 1) * 16);
   SW_DISPATCH_W(c.W(), {
     out = static_cast<u64*>(c.alloc(std::max<size_t>(l.size(), 1) * Row<W>::P * 8));
     if (!l.empty())
       relabel_kernel<W, true><<<grid_for(l.size(), 256, 148 * 8), 256, c.n() * 2, as_stream(c.stream())>>>(
-          l.words, l.cards, l.size(), c.n(), pos, out, nullptr);
+          l.words, l.cards, l.size(), c.n(), pos, out, nullptr, static_cast<ulonglong2*>(*sig));
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches++;
@@ -792,7 +828,7 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
   if (!a.empty()) {
     SW_DISPATCH_W(c.W(), {
       relabel_kernel<W, false><<<grid_for(a.size(), 256, 148 * 8), 256, n * 2, s>>>(
-          a.words, a.cards, a.size(), n, p.state_pos, sorted.words, sorted.cards);
+          a.words, a.cards, a.size(), n, p.state_pos, sorted.words, sorted.cards, nullptr);
     });
     SW_CHECK_LAUNCH();
   }
@@ -809,11 +845,12 @@ PermIndex build_perm_index(Context& c, const DList& a, StateOrder order) {
     SYNCHRO_PROGRESS("  perm-index |A|=%zu relabelled+sorted", a.size());
   }
   p.tree = build_index(c, sorted);
+  p.tree.keysig = c.alloc(std::max<size_t>(a.size(), 1) * 16);
   SW_DISPATCH_W(c.W(), {
     p.keys = static_cast<u64*>(c.alloc(std::max<size_t>(a.size(), 1) * Row<W>::P * 8));
     if (!a.empty())
-      pad_kernel<W><<<grid_for(a.size(), 256, 148 * 8), 256, 0, s>>>(sorted.words, sorted.cards, a.size(),
-                                                                    p.keys);
+      pad_kernel<W><<<grid_for(a.size(), 256, 148 * 8), 256, 0, s>>>(
+          sorted.words, sorted.cards, a.size(), p.keys, static_cast<ulonglong2*>(p.tree.keysig));
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 3;
@@ -829,7 +866,8 @@ bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
   // (Sorting the queries in relabelled-lex order was measured slower at n=570:
   // heavy walks cluster into the same warps; the (card desc, lex) level order
   // spreads them.)
-  u64* Bp = relabel_padded(c, b, p.state_pos);
+  void* Bsig = nullptr;
+  u64* Bp = relabel_padded(c, b, p.state_pos, &Bsig);
   struct Res {
     int found;
     int pad;
@@ -837,10 +875,11 @@ bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
   };
   auto* d = static_cast<Res*>(c.scratch(7, 64));
   SW_CUDA(cudaMemsetAsync(d, 0, sizeof(Res), as_stream(c.stream())));
-  launch_query<false, true>(c, p, Bp, b.size(), nullptr, &d->found, d->wit);
+  launch_query<false, true>(c, p, Bp, Bsig, b.size(), nullptr, &d->found, d->wit);
   Res h;
   c.memcpy_d2h(&h, d, sizeof(Res));
   c.free(Bp);
+  c.free(Bsig);
   if (h.found && w) {
     u32 o = 0;
     c.memcpy_d2h(&o, p.orig + h.wit[0], 4);
@@ -852,12 +891,14 @@ bool exists_subset(Context& c, const PermIndex& p, const DList& b, Witness* w) {
 
 static uint8_t* keep_flags(Context& c, const PermIndex& p, const DList& b, bool proper) {
   auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
-  u64* Bp = relabel_padded(c, b, p.state_pos);
+  void* Bsig = nullptr;
+  u64* Bp = relabel_padded(c, b, p.state_pos, &Bsig);
   if (proper)
-    launch_query<true, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
+    launch_query<true, false>(c, p, Bp, Bsig, b.size(), keep, nullptr, nullptr);
   else
-    launch_query<false, false>(c, p, Bp, b.size(), keep, nullptr, nullptr);
+    launch_query<false, false>(c, p, Bp, Bsig, b.size(), keep, nullptr, nullptr);
   c.free(Bp);
+  c.free(Bsig);
   return keep;
 }
 
@@ -886,6 +927,13 @@ size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper) {
     brute_keep_flags(c, A, b, /*super=*/false, proper, keep);
     return before - compact_flags(c, b, keep, nullptr);
   }
+  if (use_trie_index()) {
+    const size_t before = b.size();
+    const TrieQueryIndex t = build_trie_index(c, A, kTrieLeafKeys);
+    auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+    trie_superset_flags(c, t, b, proper, keep);
+    return before - compact_flags(c, b, keep, nullptr);
+  }
   const PermIndex p = build_perm_index(c, A, StateOrder::FreqDesc);
   return remove_supersets(c, p, b, proper);
 }
@@ -898,13 +946,14 @@ size_t self_reduce_minimal(Context& c, DList& l) {
     brute_keep_flags(c, l, l, /*super=*/false, /*proper=*/true, keep);
     return before - compact_flags(c, l, keep, nullptr);
   }
+  if (use_trie_index()) return trie_self_reduce_minimal(c, l);
   const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
   // The queries are the keys themselves: query with the index's own sorted,
   // relabelled rows (best locality), then map the flags back to l's order.
   const size_t before = l.size();
   auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
   uint8_t* ks = static_cast<uint8_t*>(c.alloc(l.size()));
-  launch_query<true, false>(c, p, p.keys, l.size(), ks, nullptr, nullptr);
+  launch_query<true, false>(c, p, p.keys, p.tree.keysig, l.size(), ks, nullptr, nullptr);
   scatter_flags_kernel<<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(ks, p.orig, l.size(), keep);
   SW_CHECK_LAUNCH();
   c.free(ks);

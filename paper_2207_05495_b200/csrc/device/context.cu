@@ -314,7 +314,7 @@ ContainIndex::~ContainIndex() {
   if (ctx) {
     try {
       ctx->free(nodes);
-      ctx->free(andmask);
+      ctx->free(keysig);
     } catch (...) {
     }
   }
@@ -324,14 +324,14 @@ ContainIndex& ContainIndex::operator=(ContainIndex&& o) noexcept {
   if (this != &o) {
     if (ctx) {
       ctx->free(nodes);
-      ctx->free(andmask);
+      ctx->free(keysig);
     }
     nodes = o.nodes;
-    andmask = o.andmask;
+    keysig = o.keysig;
     count = o.count;
     ctx = o.ctx;
     o.nodes = nullptr;
-    o.andmask = nullptr;
+    o.keysig = nullptr;
     o.count = 0;
   }
   return *this;

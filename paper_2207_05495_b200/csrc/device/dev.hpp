@@ -75,7 +75,7 @@ class ContainIndex {
   ContainIndex(ContainIndex&&) noexcept;
   ContainIndex& operator=(ContainIndex&&) noexcept;
   void* nodes = nullptr;    // device Node[N-1]
-  void* andmask = nullptr;  // analysis only (progress mode): per-node AND of the keys, W words
+  void* keysig = nullptr;   // per-key filter words (relabelled word 0, OR-fold), 16 B per key
   size_t count = 0;         // keys indexed
   Context* ctx = nullptr;
 };
@@ -287,6 +287,44 @@ struct TrieShape {
   std::vector<std::vector<Node>> rounds;
 };
 u64 trie_shape(Context& c, const DList& l, u32 min_leaf, TrieShape* shape);
+
+// ---- containment queries on the reference's own trie shape (trie_query.cu):
+// every internal node splits its keys on the state most of them hold
+// (static_trie.hpp:85-151), so a query lacking that state prunes the larger
+// side; payloads (an absorbed zero side, a leaf one side) are scanned.
+struct TrieNode {  // 32 B: one 256-bit load
+  u32 div, minc, zero, one;  // division state, min card, internal children (~0u: none)
+  u32 lo, mid, hi;           // key range [lo, hi): zero side [lo, mid), one side [mid, hi);
+                             // a side without an internal child is a payload to scan
+  u32 child_div;             // division states of the zero | one << 16 child (0xFFFF: none)
+};
+struct TrieQueryIndex {
+  TrieQueryIndex() = default;
+  ~TrieQueryIndex();
+  TrieQueryIndex(TrieQueryIndex&&) noexcept;
+  TrieQueryIndex& operator=(TrieQueryIndex&&) noexcept;
+  Context* ctx = nullptr;
+  size_t count = 0;         // keys
+  u64 node_count = 0;       // internal nodes (root = node 0)
+  void* nodes = nullptr;    // TrieNode[node_count]
+  u32* order = nullptr;     // key position -> index in the indexed list
+  u64* keys = nullptr;      // padded key rows in key order (card in word W)
+  void* keysig = nullptr;   // per-key filter words
+  uint8_t* state_bit = nullptr;  // state -> filter bit (the 64 most frequent key states), 255: none
+  u32 root_div = 0xFFFF;         // the root's division state (0xFFFF: the root is a leaf)
+};
+u64 build_trie_nodes(Context& c, const DList& l, u32 min_leaf, TrieQueryIndex* qi);  // internal
+TrieQueryIndex build_trie_index(Context& c, const DList& a, u32 leaf_keys);
+bool trie_exists_subset(Context& c, const TrieQueryIndex& t, const DList& b, Witness* w);
+// keep flags of b (device, |b| bytes): 0 iff b[j] is a (proper) superset of some key.
+void trie_superset_flags(Context& c, const TrieQueryIndex& t, const DList& b, bool proper,
+                         uint8_t* keep);
+// Minimal antichain through the trie index (queries = the keys, in trie order).
+size_t trie_self_reduce_minimal(Context& c, DList& l);
+// Which containment index the list paths use: the reference's trie shape
+// (default) or the relabelled radix tree (SYNCHRO_INDEX=radix, A/B only).
+bool use_trie_index();
+constexpr u32 kTrieLeafKeys = 16;
 
 // ---- microbenchmarks (microbench.cu): avg CUDA-event ms per call on `count`
 // device-generated random sets of the given density.

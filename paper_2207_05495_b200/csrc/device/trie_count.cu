@@ -168,6 +168,42 @@ __global__ void scatter_kernel(const u64* __restrict__ words, const u32* __restr
   seg_out[pos] = one ? child_one[s] : child_zero[s];
 }
 
+// Query index: the internal nodes of one round, with absolute node ids (this
+// round's first id `base`; the next round's nodes follow it) and payload ranges
+// into the final element order.
+__global__ void emit_kernel(const Seg* __restrict__ segs, u32 nact, const u32* __restrict__ div,
+                            const u32* __restrict__ zc, const u32* __restrict__ cz,
+                            const u32* __restrict__ co, const u32* __restrict__ minc, u32 base,
+                            TrieNode* __restrict__ nodes) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nact) return;
+  const Seg sg = segs[i];
+  const u32 zeros = zc[i], ones = sg.hi - sg.lo - zeros;
+  TrieNode nd;
+  nd.div = div[i];
+  nd.minc = minc[i];
+  nd.zero = cz[i] == kInvalid ? kInvalid : base + nact + cz[i];
+  nd.one = co[i] == kInvalid ? kInvalid : base + nact + co[i];
+  // a zero side of <= min_leaf sets is absorbed as payload (static_trie.hpp:107-110),
+  // a one side of <= min_leaf sets is a leaf (:84-88)
+  nd.lo = sg.lo;
+  nd.mid = sg.lo + zeros;
+  nd.hi = sg.hi;
+  nd.child_div = 0xFFFFFFFFu;  // children's division states: child_div_kernel
+  nodes[base + i] = nd;
+}
+
+// pad = the children's division states (a task carries its node's state, so
+// the query word it tests is fetched together with the node).
+__global__ void child_div_kernel(TrieNode* __restrict__ nodes, u32 count) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const TrieNode nd = nodes[i];
+  const u32 zd = nd.zero == kInvalid ? 0xFFFFu : (nodes[nd.zero].div & 0xFFFFu);
+  const u32 od = nd.one == kInvalid ? 0xFFFFu : (nodes[nd.one].div & 0xFFFFu);
+  nodes[i].child_div = zd | (od << 16);
+}
+
 __global__ void init_kernel(u32* idx, u32* seg, u32 N) {
   const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < N) {
@@ -180,8 +216,10 @@ __global__ void init_kernel(u32* idx, u32* seg, u32 N) {
 
 // Builds the trie level by level; returns the node count and, with `shape`,
 // records every internal node (division state, min cardinality, internal
-// children) round by round.
-static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape) {
+// children) round by round; with `qi`, emits the device node array of a query
+// index and the final element order (qi->order).
+static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape,
+                      TrieQueryIndex* qi = nullptr) {
   const u64 N64 = l.size();
   if (N64 == 0) throw std::invalid_argument("StaticTrie: list must be non-empty");
   min_leaf = std::max<u32>(1, min_leaf);
@@ -189,7 +227,21 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
     shape->rounds.clear();
     shape->min_leaf = min_leaf;
   }
-  if (N64 <= min_leaf) return 1;
+  if (N64 <= min_leaf) {
+    if (qi) {  // the whole list is one leaf: a pseudo node with only a payload
+      const u32 N = static_cast<u32>(N64);
+      const ListStats st = stats(c, l);
+      TrieNode root{kInvalid, st.min_card, kInvalid, kInvalid, 0, N, N, 0xFFFFFFFFu};
+      qi->nodes = c.alloc(sizeof(TrieNode));
+      c.memcpy_h2d(qi->nodes, &root, sizeof(root));
+      qi->node_count = 1;
+      qi->order = static_cast<u32*>(c.alloc(N * 4ull));
+      std::vector<u32> id(N);
+      for (u32 i = 0; i < N; ++i) id[i] = i;
+      c.memcpy_h2d(qi->order, id.data(), N * 4ull);
+    }
+    return 1;
+  }
   const u32 N = static_cast<u32>(N64), n = c.n();
   cudaStream_t s = as_stream(c.stream());
   u32* idx = static_cast<u32*>(c.alloc(N * 4ull));
@@ -215,6 +267,10 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
   u32 nact = 1;
   u32* hist = nullptr;
   size_t hist_cap = 0;
+  TrieNode* qnodes = nullptr;
+  u32 base = 0;
+  if (qi) qnodes = static_cast<TrieNode*>(c.alloc(static_cast<size_t>(N) * sizeof(TrieNode)));
+  const bool want_minc = shape || qi;
   while (nact > 0) {
     const size_t hbytes = static_cast<size_t>(nact) * n * 4;
     if (hbytes > hist_cap) {
@@ -224,7 +280,7 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
     }
     SW_CUDA(cudaMemsetAsync(hist, 0, hbytes, s));
     SW_CUDA(cudaMemsetAsync(per, 0, 6ull * max_segs * 4, s));
-    u32* minc = shape ? per + 6ull * max_segs : nullptr;
+    u32* minc = want_minc ? per + 6ull * max_segs : nullptr;
     if (minc) SW_CUDA(cudaMemsetAsync(minc, 0xFF, static_cast<size_t>(nact) * 4, s));
     SW_CUDA(cudaMemsetAsync(&ctr->next_count, 0, 4, s));
     u32* div = per;
@@ -243,6 +299,10 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
       scatter_kernel<W><<<(N + 255) / 256, 256, 0, s>>>(l.words, idx, seg, N, segs, div, zc, cz, co,
                                                         curz, curo, idx2, seg2);
     });
+    if (qi) {
+      emit_kernel<<<(nact + 255) / 256, 256, 0, s>>>(segs, nact, div, zc, cz, co, minc, base, qnodes);
+      base += nact;
+    }
     SW_CHECK_LAUNCH();
     c.counters.kernel_launches += 3;
     if (shape) {
@@ -262,6 +322,14 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
     c.memcpy_d2h(&h, ctr, sizeof(h));
     nact = h.next_count;
   }
+  if (qi) {  // elements of every node's range are contiguous in idx
+    child_div_kernel<<<(base + 255) / 256, 256, 0, s>>>(qnodes, base);
+    SW_CHECK_LAUNCH();
+    qi->nodes = qnodes;
+    qi->node_count = base;
+    qi->order = idx;
+    idx = nullptr;
+  }
   c.free(idx);
   c.free(seg);
   c.free(idx2);
@@ -280,6 +348,10 @@ u64 trie_node_count(Context& c, const DList& l, u32 min_leaf) { return build_tri
 
 u64 trie_shape(Context& c, const DList& l, u32 min_leaf, TrieShape* shape) {
   return build_trie(c, l, min_leaf, shape);
+}
+
+u64 build_trie_nodes(Context& c, const DList& l, u32 min_leaf, TrieQueryIndex* qi) {
+  return build_trie(c, l, min_leaf, nullptr, qi);
 }
 
 }  // namespace synchro::dev

@@ -1,0 +1,581 @@
+// Containment queries on the reference's own trie shape.
+//
+// The reference answers "does some stored set lie inside query y" with its
+// StaticTrie (static_trie.hpp:26-188): every node splits its sets on the state
+// most of them hold (ties to the smallest state), the zero side (sets without
+// it) is always admissible, the one side only to queries holding the state;
+// small sides are payloads scanned pair by pair, and a node whose min
+// cardinality exceeds |y| is cut.  Splitting on the locally most frequent
+// state makes the pruned one side as large as possible — for the sparse sets
+// of the search a query usually lacks the state and drops the larger half.
+//
+// Here the same shape is built level-synchronously on the GPU
+// (trie_count.cu, the ledger's node count builder, emitting nodes), its keys
+// are stored in the trie's own order (every node's keys contiguous), and
+// queries walk it with the warp work pool of contain.cu: a task is (query,
+// node); a round loads the node, the query row and its filter words at once;
+// payload ranges of the round's tasks are flattened over the lanes and each
+// (key, query) pair first compares 16-byte filter words.
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "dev.hpp"
+#include "kernels.cuh"
+#include "util.cuh"
+#include "../progress.hpp"
+
+namespace synchro::dev {
+
+namespace {
+
+constexpr u32 kNo = 0xFFFFFFFFu;
+constexpr int kWarps = 6;
+constexpr int kThreads = kWarps * 32;
+constexpr int kCap = 256;        // tasks per warp in shared memory
+constexpr int kSpillHalf = kCap / 2;
+constexpr int kSpillCap = 1024;  // tasks per warp in the global spill stack
+constexpr int kHitSlots = 32;
+
+template <int W>
+struct Pad {
+  static constexpr int P = (W + 2) & ~1;  // padded row: W words + the card
+};
+
+__device__ __forceinline__ TrieNode load_trie_node(const TrieNode* p) {
+  unsigned long long w0, w1, w2, w3;
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(p));
+  TrieNode t;
+  t.div = static_cast<u32>(w0);
+  t.minc = static_cast<u32>(w0 >> 32);
+  t.zero = static_cast<u32>(w1);
+  t.one = static_cast<u32>(w1 >> 32);
+  t.lo = static_cast<u32>(w2);
+  t.mid = static_cast<u32>(w2 >> 32);
+  t.hi = static_cast<u32>(w3);
+  t.child_div = static_cast<u32>(w3 >> 32);
+  return t;
+}
+
+template <int W>
+__device__ __forceinline__ void load_prow(const u64* __restrict__ base, u64 idx, u64 (&x)[W],
+                                          u32& card) {
+  constexpr int P = Pad<W>::P;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(base + idx * P);
+#pragma unroll
+  for (int i = 0; i < P / 2; ++i) {
+    const ulonglong2 v = __ldg(p + i);
+    if (2 * i < W) x[2 * i] = v.x;
+    if (2 * i == W) card = static_cast<u32>(v.x);
+    if (2 * i + 1 < W) x[2 * i + 1] = v.y;
+    if (2 * i + 1 == W) card = static_cast<u32>(v.y);
+  }
+}
+
+__device__ __forceinline__ bool sig_pass(ulonglong2 x, ulonglong2 y) {
+  return ((x.x & ~y.x) | (x.y & ~y.y)) == 0;
+}
+
+// Padded rows + filter words {bits of the 64 most frequent key states, OR-fold}
+// (both monotone: x ⊆ y implies sig(x) ⊆ sig(y) word by word).  Row i is
+// src[order[i]] when order is given.
+template <int W>
+__global__ void trie_pad_kernel(const u64* __restrict__ src, const u32* __restrict__ scard,
+                                const u32* __restrict__ order, u64 count, u32 n,
+                                const uint8_t* __restrict__ g_bit, u64* __restrict__ dst,
+                                ulonglong2* __restrict__ dsig) {
+  extern __shared__ uint8_t s_bit[];
+  for (u32 q = threadIdx.x; q < n; q += blockDim.x) s_bit[q] = g_bit[q];
+  __syncthreads();
+  constexpr int P = Pad<W>::P;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 r = order ? order[i] : i;
+    u64 x[W];
+    u64 fold = 0, top = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      x[w] = src[r * W + w];
+      fold |= x[w];
+      u64 bits = x[w];
+      while (bits) {
+        const int b = __clzll(bits);
+        bits &= ~(u64{1} << (63 - b));
+        const uint8_t t = s_bit[w * 64 + b];
+        if (t != 255) top |= u64{1} << t;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < P; ++w) dst[i * P + w] = w < W ? x[w] : (w == W ? scard[r] : 0);
+    dsig[i] = make_ulonglong2(top, fold);
+  }
+}
+
+__global__ void map_flags_kernel(const uint8_t* __restrict__ src, const u32* __restrict__ perm,
+                                 u64 count, uint8_t* __restrict__ dst) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    dst[perm[i]] = src[i];
+}
+
+// Warp work pool over (query, node) tasks.  MARK: keep[j] = 0 for queries with
+// a (proper) subset among the keys; EXIST: *found / wit on the first hit.
+template <int W, bool PROPER, bool EXIST>
+__global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) trie_pool_kernel(
+    const u64* __restrict__ K, const ulonglong2* __restrict__ Ksig,
+    const TrieNode* __restrict__ nodes, const u64* __restrict__ Q,
+    const ulonglong2* __restrict__ Qsig, u32 Nq, uint8_t* keep, int* found,
+    unsigned long long* wit, u32* next_query, uint4* spill_all, u32* overflow_scans,
+    unsigned long long* stats, u32 root_div, u32 spill_cap) {
+  constexpr int P = Pad<W>::P;
+  __shared__ u32 s_q[kWarps][kCap];
+  __shared__ u32 s_n[kWarps][kCap];
+  __shared__ u32 s_c[kWarps][kCap];
+  __shared__ u32 s_hit[kWarps][kHitSlots];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned FULL = 0xFFFFFFFFu, lt = (1u << lane) - 1;
+  u32* sq = s_q[wid];
+  u32* sn = s_n[wid];
+  u32* sc = s_c[wid];
+  u32* shit = s_hit[wid];
+  shit[lane] = kNo;
+  __syncwarp();
+  uint4* spill = spill_all + (static_cast<u64>(blockIdx.x) * kWarps + wid) * kSpillCap;
+  int sp = 0, gsp = 0;
+  bool more = true;
+  int found_seen = 0;
+  auto report = [&](u32 key, u32 q) {
+    if (EXIST) {
+      if (atomicCAS(found, 0, 1) == 0) {
+        wit[0] = key;
+        wit[1] = q;
+      }
+    } else {
+      keep[q] = 0;
+      shit[q % kHitSlots] = q;
+    }
+  };
+  while (true) {
+    if (EXIST) {  // read one round ahead (its latency overlaps a round of work)
+      if (found_seen) break;
+      found_seen = *reinterpret_cast<volatile int*>(found);
+    }
+    if (sp < 32 && gsp > 0) {
+      const int t = gsp < kSpillHalf ? gsp : kSpillHalf;
+      for (int i = lane; i < t; i += 32) {
+        const uint4 v = spill[gsp - t + i];
+        sq[sp + i] = v.x;
+        sn[sp + i] = v.y;
+        sc[sp + i] = v.z;
+      }
+      gsp -= t;
+      sp += t;
+      __syncwarp();
+    } else if (sp < 32 && more) {
+      u32 base = 0;
+      if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
+      base = __shfl_sync(FULL, base, 0);
+      const u32 got = base >= Nq ? 0 : min(static_cast<u32>(32 - sp), Nq - base);
+      if (base + (32 - sp) >= Nq) more = false;
+      const u32 j = base + lane;
+      bool push = static_cast<u32>(lane) < got;
+      const u32 cy = push ? static_cast<u32>(Q[static_cast<u64>(j) * P + W]) : 0;
+      if (PROPER && cy == 0) push = false;
+      const unsigned m = __ballot_sync(FULL, push);
+      if (push) {
+        const int pos = sp + __popc(m & lt);
+        sq[pos] = j;
+        sn[pos] = 0;  // root
+        sc[pos] = cy | (root_div << 16);
+      }
+      sp += __popc(m);
+      __syncwarp();
+    }
+    if (sp == 0) {
+      if (!more && gsp == 0) break;
+      continue;
+    }
+    const int take = sp < 32 ? sp : 32;
+    bool have = lane < take;
+    u32 j = 0, id = 0, cy = 0, dv = 0xFFFF;
+    if (have) {
+      const int pos = sp - 1 - lane;
+      j = sq[pos];
+      id = sn[pos];
+      cy = sc[pos] & 0xFFFF;
+      dv = sc[pos] >> 16;  // the node's division state, carried by the task
+    }
+    sp -= take;
+    __syncwarp();
+    if (!EXIST && have && shit[j % kHitSlots] == j) have = false;
+    const u32 limit = PROPER ? cy - 1 : cy;
+
+    // ---- one round of independent loads: the node, the query's filter words
+    // and the query word holding the node's division state (carried by the task)
+    TrieNode nd{};
+    ulonglong2 qs = make_ulonglong2(0, 0);
+    u64 yw = 0;
+    if (have) {
+      nd = load_trie_node(nodes + id);
+      qs = __ldg(Qsig + j);
+      if (dv != 0xFFFF) yw = __ldg(Q + static_cast<u64>(j) * P + (dv >> 6));
+    }
+    // ---- evaluate: zero side always, one side iff y holds the division state
+    u32 c0 = kNo, c1 = kNo, zlo = 0, zn = 0, olo = 0, on = 0;
+    if (have && nd.minc <= limit) {
+      if (nd.zero != kNo) {
+        c0 = nd.zero;
+      } else {
+        zlo = nd.lo;
+        zn = nd.mid - nd.lo;
+      }
+      if (dv != 0xFFFF) {
+        if ((yw >> (63 - (dv & 63))) & 1) {
+          if (nd.one != kNo) {
+            c1 = nd.one;
+          } else {
+            olo = nd.mid;
+            on = nd.hi - nd.mid;
+          }
+        }
+      }
+    }
+    if (stats) {
+      const u32 v[3] = {static_cast<u32>(__popc(__ballot_sync(FULL, have))),
+                        static_cast<u32>(__popc(__ballot_sync(FULL, c0 != kNo))),
+                        static_cast<u32>(__popc(__ballot_sync(FULL, c1 != kNo)))};
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) atomicAdd(stats + q, static_cast<unsigned long long>(v[q]));
+      }
+    }
+    // ---- push children
+    const unsigned m0 = __ballot_sync(FULL, c0 != kNo);
+    const unsigned m1 = __ballot_sync(FULL, c1 != kNo);
+    const int n0 = __popc(m0), n1 = __popc(m1);
+    if (sp + n0 + n1 > kCap && gsp + kSpillHalf <= static_cast<int>(spill_cap)) {
+      for (int i = lane; i < kSpillHalf; i += 32) spill[gsp + i] = make_uint4(sq[i], sn[i], sc[i], 0);
+      __syncwarp();
+      for (int i = lane; i < sp - kSpillHalf; i += 32) {
+        sq[i] = sq[i + kSpillHalf];
+        sn[i] = sn[i + kSpillHalf];
+        sc[i] = sc[i + kSpillHalf];
+      }
+      __syncwarp();
+      gsp += kSpillHalf;
+      sp -= kSpillHalf;
+    }
+    if (sp + n0 + n1 > kCap) {  // pool and spill stack full: scan the children's ranges
+      if (c0 != kNo) {
+        zlo = nd.lo;
+        zn = nd.mid - nd.lo;
+      }
+      if (c1 != kNo) {
+        olo = nd.mid;
+        on = nd.hi - nd.mid;
+      }
+      if (lane == 0) atomicAdd(overflow_scans, 1u);
+    } else {
+      if (c1 != kNo) {
+        const int pos = sp + __popc(m1 & lt);
+        sq[pos] = j;
+        sn[pos] = c1;
+        sc[pos] = cy | (nd.child_div & 0xFFFF0000u);
+      }
+      if (c0 != kNo) {
+        const int pos = sp + n1 + __popc(m0 & lt);
+        sq[pos] = j;
+        sn[pos] = c0;
+        sc[pos] = cy | (nd.child_div << 16);
+      }
+      sp += n0 + n1;
+    }
+    __syncwarp();
+
+    // ---- payload scan: (key, query) pairs of the round flattened over lanes
+    const u32 cnt = zn + on;
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const u32 total = __shfl_sync(FULL, incl, 31);
+    if (stats && lane == 0) atomicAdd(stats + 3, static_cast<unsigned long long>(total));
+    const u32 excl = incl - cnt;
+    for (u32 base = 0; base < total; base += 32) {
+      const u32 t = base + lane;
+      int owner = 0;
+#pragma unroll
+      for (int s = 16; s; s >>= 1) {
+        const u32 v = __shfl_sync(FULL, incl, owner + s - 1);
+        if (v <= t) owner += s;
+      }
+      owner = owner > 31 ? 31 : owner;
+      const u32 o_excl = __shfl_sync(FULL, excl, owner);
+      const u32 o_zlo = __shfl_sync(FULL, zlo, owner);
+      const u32 o_zn = __shfl_sync(FULL, zn, owner);
+      const u32 o_olo = __shfl_sync(FULL, olo, owner);
+      const u32 o_j = __shfl_sync(FULL, j, owner);
+      const u32 o_lim = __shfl_sync(FULL, limit, owner);
+      const ulonglong2 oq = make_ulonglong2(__shfl_sync(FULL, qs.x, owner),
+                                            __shfl_sync(FULL, qs.y, owner));
+      if (t < total) {
+        const u32 r = t - o_excl;
+        const u32 key = r < o_zn ? o_zlo + r : o_olo + (r - o_zn);
+        if (sig_pass(__ldg(Ksig + key), oq)) {  // rare: the exact test
+          const u64* kr = K + static_cast<u64>(key) * P;
+          const u64* yr = Q + static_cast<u64>(o_j) * P;
+          u64 acc = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc |= __ldg(kr + w) & ~__ldg(yr + w);
+          if (static_cast<u32>(__ldg(kr + W)) <= o_lim && acc == 0) report(key, o_j);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Padded query rows + filter words of b under the index's state map.
+template <int W>
+u64* pad_queries(Context& c, const TrieQueryIndex& t, const DList& b, const u32* order,
+                 void** sig) {
+  u64* rows = static_cast<u64*>(c.alloc(std::max<size_t>(b.size(), 1) * Pad<W>::P * 8));
+  *sig = c.alloc(std::max<size_t>(b.size(), 1) * 16);
+  if (!b.empty())
+    trie_pad_kernel<W><<<grid_for(b.size(), 256, 148 * 8), 256, c.n(), as_stream(c.stream())>>>(
+        b.words, b.cards, order, b.size(), c.n(), t.state_bit, rows, static_cast<ulonglong2*>(*sig));
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+  return rows;
+}
+
+template <bool PROPER, bool EXIST>
+void launch(Context& c, const TrieQueryIndex& t, const u64* Qrows, const void* Qsig, u64 Nq,
+            uint8_t* keep, int* found, unsigned long long* wit) {
+  if (!Nq) return;
+  cudaStream_t s = as_stream(c.stream());
+  if (!EXIST) SW_CUDA(cudaMemsetAsync(keep, 1, Nq, s));
+  if (t.count == 0) return;
+  u32* counter = static_cast<u32*>(c.scratch(7, 64)) + 8;
+  SW_CUDA(cudaMemsetAsync(counter, 0, 8, s));
+  static std::atomic<int> cache_bps[kMaxW + 1];
+  static std::atomic<int> cache_sms{0};
+  int sms = cache_sms.load(std::memory_order_relaxed);
+  if (!sms) {
+    int dev = 0;
+    SW_CUDA(cudaGetDevice(&dev));
+    SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cache_sms.store(sms, std::memory_order_relaxed);
+  }
+  int bps = cache_bps[c.W()].load(std::memory_order_relaxed);
+  if (!bps) {
+    SW_DISPATCH_W(c.W(), {
+      SW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &bps, trie_pool_kernel<W, PROPER, EXIST>, kThreads, 0));
+    });
+    bps = std::max(1, bps);
+    cache_bps[c.W()].store(bps, std::memory_order_relaxed);
+  }
+  const u64 want = (Nq + kThreads - 1) / kThreads;
+  const unsigned grid =
+      static_cast<unsigned>(std::max<u64>(1, std::min<u64>(want, static_cast<u64>(sms) * bps)));
+  unsigned long long* stats = nullptr;
+  if (progress_enabled() || c.contain_stats) {
+    stats = static_cast<unsigned long long*>(c.scratch(7, 64 + 9 * 8)) + 8;
+    SW_CUDA(cudaMemsetAsync(stats, 0, 9 * 8, s));
+  }
+  uint4* spill = static_cast<uint4*>(
+      c.scratch(10, static_cast<size_t>(grid) * kWarps * kSpillCap * sizeof(uint4)));
+  // Test hook (as contain.cu): SYNCHRO_SPILL_CAP shrinks the spill stack so the
+  // overflow scan path runs.
+  const u32 spill_cap = [] {
+    const char* e = std::getenv("SYNCHRO_SPILL_CAP");
+    const long v = e && *e ? std::strtol(e, nullptr, 10) : kSpillCap;
+    return static_cast<u32>(std::clamp<long>(v, 0, kSpillCap));
+  }();
+  std::unique_ptr<StreamTimer> timer;
+  if (progress_enabled() || c.timing) {
+    timer = std::make_unique<StreamTimer>(c);
+    timer->start();
+  }
+  SW_DISPATCH_W(c.W(), {
+    trie_pool_kernel<W, PROPER, EXIST><<<grid, kThreads, 0, s>>>(
+        t.keys, static_cast<const ulonglong2*>(t.keysig), static_cast<const TrieNode*>(t.nodes),
+        Qrows, static_cast<const ulonglong2*>(Qsig), static_cast<u32>(Nq), keep, found, wit,
+        counter, spill, counter + 1, stats, t.root_div, spill_cap);
+  });
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 1;
+  if (timer) {
+    const double ms = timer->stop_ms();
+    const u64 row = static_cast<u64>(c.W()) * 8 + 4;
+    c.counters.contain_ms += ms;
+    c.counters.contain_launches += 1;
+    c.counters.contain_bytes += (t.count + Nq) * row + (EXIST ? 0 : Nq);
+    if (progress_enabled()) {
+      u32 overflow = 0;
+      c.memcpy_d2h(&overflow, counter + 1, 4);
+      unsigned long long st[4];
+      c.memcpy_d2h(st, stats, sizeof(st));
+      SYNCHRO_PROGRESS("  trie-stats tasks=%llu push0=%llu push1=%llu pairs=%llu", st[0], st[1],
+                       st[2], st[3]);
+      SYNCHRO_PROGRESS("  contain %s%s |A|=%zu |B|=%llu %.3f ms overflow_scans=%u",
+                       EXIST ? "exist" : "mark", PROPER ? "-proper" : "", t.count,
+                       static_cast<unsigned long long>(Nq), ms, overflow);
+    }
+  }
+  if (c.contain_stats) {
+    unsigned long long st[4];
+    c.memcpy_d2h(st, stats, sizeof(st));
+    c.counters.contain_visits += st[0];
+    c.counters.contain_pairs += st[3];
+  }
+}
+
+}  // namespace
+
+TrieQueryIndex::~TrieQueryIndex() {
+  if (ctx) {
+    try {
+      ctx->free(nodes);
+      ctx->free(order);
+      ctx->free(keys);
+      ctx->free(keysig);
+      ctx->free(state_bit);
+    } catch (...) {
+    }
+  }
+}
+TrieQueryIndex::TrieQueryIndex(TrieQueryIndex&& o) noexcept { *this = std::move(o); }
+TrieQueryIndex& TrieQueryIndex::operator=(TrieQueryIndex&& o) noexcept {
+  if (this != &o) {
+    if (ctx) {
+      ctx->free(nodes);
+      ctx->free(order);
+      ctx->free(keys);
+      ctx->free(keysig);
+      ctx->free(state_bit);
+    }
+    ctx = o.ctx;
+    count = o.count;
+    node_count = o.node_count;
+    nodes = o.nodes;
+    order = o.order;
+    keys = o.keys;
+    keysig = o.keysig;
+    state_bit = o.state_bit;
+    root_div = o.root_div;
+    o.ctx = nullptr;
+    o.nodes = nullptr;
+    o.order = nullptr;
+    o.keys = nullptr;
+    o.keysig = nullptr;
+    o.state_bit = nullptr;
+    o.count = 0;
+  }
+  return *this;
+}
+
+TrieQueryIndex build_trie_index(Context& c, const DList& a, u32 leaf_keys) {
+  TrieQueryIndex t;
+  t.ctx = &c;
+  t.count = a.size();
+  const u32 n = c.n();
+  // filter bit map: the 64 most frequent states of the keys
+  std::vector<uint8_t> bit(n, 255);
+  if (!a.empty()) {
+    u32* hist = static_cast<u32*>(c.alloc(n * 4));
+    state_histogram(c, a, hist);
+    std::vector<u32> h(n);
+    c.memcpy_d2h(h.data(), hist, n * 4);
+    c.free(hist);
+    std::vector<u32> ord(n);
+    for (u32 q = 0; q < n; ++q) ord[q] = q;
+    std::stable_sort(ord.begin(), ord.end(), [&](u32 x, u32 y) { return h[x] > h[y]; });
+    for (u32 i = 0; i < std::min<u32>(64, n); ++i) bit[ord[i]] = static_cast<uint8_t>(i);
+  }
+  t.state_bit = static_cast<uint8_t*>(c.alloc(std::max<u32>(n, 1)));
+  c.memcpy_h2d(t.state_bit, bit.data(), n);
+  if (a.empty()) return t;
+  build_trie_nodes(c, a, leaf_keys, &t);
+  TrieNode root{};
+  c.memcpy_d2h(&root, t.nodes, sizeof(root));
+  t.root_div = root.div == 0xFFFFFFFFu ? 0xFFFFu : root.div;
+  SW_DISPATCH_W(c.W(), {
+    void* sig = nullptr;
+    t.keys = pad_queries<W>(c, t, a, t.order, &sig);
+    t.keysig = sig;
+  });
+  SYNCHRO_PROGRESS("  trie-index |A|=%zu nodes=%llu", a.size(),
+                   static_cast<unsigned long long>(t.node_count));
+  return t;
+}
+
+bool trie_exists_subset(Context& c, const TrieQueryIndex& t, const DList& b, Witness* w) {
+  if (t.count == 0 || b.empty()) return false;
+  void* sig = nullptr;
+  u64* rows = nullptr;
+  SW_DISPATCH_W(c.W(), { rows = pad_queries<W>(c, t, b, nullptr, &sig); });
+  struct Res {
+    int found;
+    int pad;
+    unsigned long long wit[2];
+  };
+  auto* d = static_cast<Res*>(c.scratch(7, 64));
+  SW_CUDA(cudaMemsetAsync(d, 0, sizeof(Res), as_stream(c.stream())));
+  launch<false, true>(c, t, rows, sig, b.size(), nullptr, &d->found, d->wit);
+  Res h;
+  c.memcpy_d2h(&h, d, sizeof(Res));
+  c.free(rows);
+  c.free(sig);
+  if (h.found && w) {
+    u32 o = 0;
+    c.memcpy_d2h(&o, t.order + h.wit[0], 4);
+    w->a_index = o;
+    w->b_index = h.wit[1];
+  }
+  return h.found != 0;
+}
+
+void trie_superset_flags(Context& c, const TrieQueryIndex& t, const DList& b, bool proper,
+                         uint8_t* keep) {
+  if (b.empty()) return;
+  void* sig = nullptr;
+  u64* rows = nullptr;
+  SW_DISPATCH_W(c.W(), { rows = pad_queries<W>(c, t, b, nullptr, &sig); });
+  if (proper)
+    launch<true, false>(c, t, rows, sig, b.size(), keep, nullptr, nullptr);
+  else
+    launch<false, false>(c, t, rows, sig, b.size(), keep, nullptr, nullptr);
+  c.free(rows);
+  c.free(sig);
+}
+
+size_t trie_self_reduce_minimal(Context& c, DList& l) {
+  if (l.size() <= 1) return 0;
+  const size_t before = l.size();
+  const TrieQueryIndex t = build_trie_index(c, l, kTrieLeafKeys);
+  auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
+  uint8_t* kt = static_cast<uint8_t*>(c.alloc(l.size()));
+  // queries = the keys themselves in trie order (neighbours share paths)
+  launch<true, false>(c, t, t.keys, t.keysig, l.size(), kt, nullptr, nullptr);
+  map_flags_kernel<<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(kt, t.order, l.size(),
+                                                                               keep);
+  SW_CHECK_LAUNCH();
+  c.free(kt);
+  return before - compact_flags(c, l, keep, nullptr);
+}
+
+bool use_trie_index() {
+  static const bool on = [] {
+    const char* e = std::getenv("SYNCHRO_INDEX");
+    return !(e && std::string(e) == "radix");
+  }();
+  return on;
+}
+
+}  // namespace synchro::dev

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <functional>
 #include <cstdlib>
 #include <set>
 #include <sstream>
@@ -153,6 +154,21 @@ const dev::PermIndex& GpuBibfs::bfs_index() {
   return *lbfs_index_;
 }
 
+// The reference's own trie shape over L_BFS (static_trie.hpp:26-151) as the
+// query structure of the meet check and the DFS (device/trie_query.cu).
+const dev::TrieQueryIndex& GpuBibfs::bfs_trie() {
+  if (!lbfs_trie_)
+    lbfs_trie_ = std::make_unique<dev::TrieQueryIndex>(
+        dev::build_trie_index(ctx_, *lbfs_, dev::kTrieLeafKeys));
+  return *lbfs_trie_;
+}
+
+// Is some L_BFS set a subset of some set of b?  (meet_check / trie query)
+bool GpuBibfs::exists_in_bfs(const DList& b, dev::Witness* w) {
+  if (dev::use_trie_index()) return dev::trie_exists_subset(ctx_, bfs_trie(), b, w);
+  return dev::exists_subset(ctx_, bfs_index(), b, w);
+}
+
 namespace {
 // Releases the charged layer if a step aborts between expansion and commit
 // (bibfs_engine.hpp:334-343).
@@ -212,6 +228,7 @@ void GpuBibfs::bfs_step(bool with_history) {
   lbfs_met_ = false;
   *lbfs_ = std::move(next);
   lbfs_index_.reset();
+  lbfs_trie_.reset();
   refresh(*lbfs_, lbfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
@@ -294,14 +311,14 @@ bool GpuBibfs::meet() {
   lbfs_met_ = !opt_.track_word;  // meet_check permutes L_IBFS (subset_algebra.hpp:201-210)
   if (dev::brute_fits(lbfs_->size(), libfs_->size()))
     return dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, nullptr);
-  return dev::exists_subset(ctx_, bfs_index(), *libfs_, nullptr);
+  return exists_in_bfs(*libfs_, nullptr);
 }
 
 bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
   dev::Witness w;
   const bool met = dev::brute_fits(lbfs_->size(), libfs_->size())
                        ? dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, &w)
-                       : dev::exists_subset(ctx_, bfs_index(), *libfs_, &w);
+                       : exists_in_bfs(*libfs_, &w);
   if (!met) return false;
   *bfs_index_out = w.a_index;
   *ibfs_tag = dev::read_tag(ctx_, *libfs_, w.b_index);
@@ -363,10 +380,11 @@ void dump_list(dev::Context& c, const DList& l, const std::string& name) {
 // query against L_BFS are device kernels.
 class DfsRunner {
  public:
-  DfsRunner(dev::Context& c, const DList& lbfs, const dev::PermIndex& index,
-            MemoryLedger& ledger, const EngineTuning& t, const Deadline& deadline, bool tracking,
+  using Query = std::function<bool(const DList&, dev::Witness*)>;
+  DfsRunner(dev::Context& c, const DList& lbfs, Query query, MemoryLedger& ledger,
+            const EngineTuning& t, const Deadline& deadline, bool tracking,
             std::vector<std::array<u64, 5>>* log)
-      : c_(c), lbfs_(lbfs), index_(index), ledger_(ledger), t_(t), deadline_(deadline),
+      : c_(c), lbfs_(lbfs), query_(std::move(query)), ledger_(ledger), t_(t), deadline_(deadline),
         tracking_(tracking), log_(log) {}
 
   // Shard s of c explores the subtrees of initial[i] for i ≡ s (mod c) only
@@ -444,7 +462,7 @@ class DfsRunner {
                      static_cast<unsigned long long>(r), level, hi - lo,
                      static_cast<unsigned long long>(generated), next.size());
     dev::Witness w;
-    if (dev::exists_subset(c_, index_, next, tracking_ ? &w : nullptr)) {
+    if (query_(next, tracking_ ? &w : nullptr)) {
       bound_ = r;
       if (tracking_) record_find(w, next, parent);
       return;
@@ -520,7 +538,7 @@ class DfsRunner {
 
   dev::Context& c_;
   const DList& lbfs_;
-  const dev::PermIndex& index_;
+  Query query_;
   MemoryLedger& ledger_;
   const EngineTuning& t_;
   const Deadline& deadline_;
@@ -553,8 +571,8 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
     replay_meet_order();
   dump_list(ctx_, *lbfs_, "lbfs");
   dump_list(ctx_, *libfs_, "libfs");
-  const dev::PermIndex& index = bfs_index();
-  DfsRunner dfs(ctx_, *lbfs_, index, ledger_, opt_.tuning, deadline_, opt_.track_word, log);
+  DfsRunner dfs(ctx_, *lbfs_, [this](const DList& b, dev::Witness* w) { return exists_in_bfs(b, w); },
+                ledger_, opt_.tuning, deadline_, opt_.track_word, log);
   const u64 final_bound =
       dfs.run(*libfs_, r, R_, opt_.dfs_shard_index, std::max<u32>(1, opt_.dfs_shard_count));
   if (find) *find = dfs.find();

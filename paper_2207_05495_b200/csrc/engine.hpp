@@ -21,11 +21,15 @@
 
 namespace synchro {
 
+class Comm;
+
 namespace dev {
 class Context;
 class DList;
 struct ContainIndex;
 struct PermIndex;
+struct TrieQueryIndex;
+struct Witness;
 }  // namespace dev
 
 enum class Schedule { Auto, BfsOnly, IbfsOnly, DfsImmediate };
@@ -62,6 +66,8 @@ struct SolveOptions {
   // Analysis / prefix-parity hook: stop before iteration stop_after_iterations+1
   // (phase "stopped", threshold 0).  0 = run to the end.
   u64 stop_after_iterations = 0;
+  // Partitioned solve over several GPUs (comm.hpp; not owned).  nullptr: one GPU.
+  Comm* comm = nullptr;
 };
 
 struct SolveResult {
@@ -145,6 +151,8 @@ class GpuBibfs {
   void shrink_charge(size_t now_size);
   void merge_history(dev::DList& h, Info& hi, const dev::DList& add);
   const dev::PermIndex& bfs_index();
+  const dev::TrieQueryIndex& bfs_trie();
+  bool exists_in_bfs(const dev::DList& b, dev::Witness* w);
 
   const Automaton& aut_;
   const SolveOptions& opt_;
@@ -156,6 +164,7 @@ class GpuBibfs {
   u64 r_ = 0;
   std::unique_ptr<dev::DList> lbfs_, libfs_, hbfs_, hibfs_c_;
   std::unique_ptr<dev::PermIndex> lbfs_index_;
+  std::unique_ptr<dev::TrieQueryIndex> lbfs_trie_;
   Info lbfs_i_, libfs_i_, hbfs_i_, hibfs_i_;
   size_t h_bfs_last_reduced_ = 1, h_ibfs_last_reduced_ = 1;
   bool bfs_hist_dropped_ = false, ibfs_hist_dropped_ = false;

@@ -34,7 +34,8 @@ EXPORTED_SYMBOLS = [
     "sw_list_dedupe_sorted", "sw_list_hash_dedupe", "sw_list_self_reduce_minimal", "sw_list_mark",
     "sw_list_meet_check", "sw_trie_node_count", "sw_run_experiment", "sw_exp_mark",
     "sw_step_costs", "sw_bench_expand", "sw_bench_dedupe", "sw_dev_owner_partition",
-    "sw_dev_hash_dedupe", "sw_solve_exact_ex", "sw_meet_check_order",
+    "sw_dev_hash_dedupe", "sw_solve_exact_ex", "sw_meet_check_order", "sw_list_trie_exists",
+    "sw_nccl_unique_id", "sw_comm_create", "sw_comm_destroy", "sw_solve_exact_dist",
 ]
 
 
@@ -137,6 +138,9 @@ def load():
     L.sw_solve_exact_ex.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(SolveOptions),
                                     C.POINTER(SolveResultC), C.c_void_p, C.c_size_t, C.c_char_p,
                                     C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.sw_list_trie_exists.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64)]
     L.sw_meet_check_order.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
                                       C.c_uint32, _u32p]
     L.sw_heuristic.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_int32, C.c_uint64, C.c_uint64,
@@ -373,6 +377,17 @@ def solve_exact(aut: Automaton, trace_path: Optional[str] = None, **opts) -> Sol
                        r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
                        r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace,
                        r.contain_visits, r.contain_pairs, dfs_levels)
+
+
+def list_trie_exists(n: int, a_words, b_words):
+    """(met, a_index, b_index) through the trie index (a in any order)."""
+    W = (n + 63) // 64
+    a = np.ascontiguousarray(a_words, np.uint64)
+    b = np.ascontiguousarray(b_words, np.uint64)
+    m, ai, bi = C.c_int32(), C.c_uint64(), C.c_uint64()
+    _check(load().sw_list_trie_exists(n, a, a.size // W, b, b.size // W, C.byref(m), C.byref(ai),
+                                      C.byref(bi)))
+    return bool(m.value), int(ai.value), int(bi.value)
 
 
 def meet_check_order(n: int, a_words, b_words, min_brute: int = 64) -> np.ndarray:

@@ -315,3 +315,22 @@ def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap):
     assert "BAD []" in p.stdout, p.stdout
     scans = [int(x) for x in __import__("re").findall(r"overflow_scans=(\d+)", p.stderr)]
     assert scans and max(scans) > 0, "overflow path not exercised"
+
+
+@pytest.mark.parametrize("n,da,db,seed", [(100, 0.1, 0.4, 0), (300, 0.08, 0.3, 1), (64, 0.3, 0.3, 3)])
+def test_trie_exists_any_key_order(gpu, ref, n, da, db, seed):
+    """The trie index (device/trie_query.cu) over keys in ANY order (the engine
+    indexes L_BFS in hash order): one planted containment is found wherever it
+    lies, including under the root's one side."""
+    keys = lex_sorted_unique(n, random_list(n, 5000, da, seed)).reshape(-1, W(n))
+    rng = np.random.default_rng(seed)
+    keys = keys[rng.permutation(len(keys))]
+    b = random_list(n, 1500, db, seed + 7).reshape(-1, W(n)).copy()
+    met, _, _ = gpu.list_trie_exists(n, keys.reshape(-1), b.reshape(-1))
+    assert met == ref.meet_check(n, lex_sorted_unique(n, keys.reshape(-1)), b.reshape(-1))
+    for pick in (0, len(keys) // 2, len(keys) - 1):
+        b2 = b.copy()
+        b2[17] |= keys[pick]
+        met, ai, bi = gpu.list_trie_exists(n, keys.reshape(-1), b2.reshape(-1))
+        assert met
+        assert np.all((keys[ai] & ~b2[bi]) == 0)
