@@ -12,8 +12,9 @@ included (solve_exact(aut) from a host transition table, result word read back).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 (torchrun): every rank solves an independent replica of the workload on
-its own GPU (no data-path collective) — `value` is the aggregate.
+N>1 (torchrun): ONE solve of the workload partitioned over the N GPUs by hash
+ownership (sw_solve_exact_dist over NCCL) — `value` is the job's
+expansions over the max-over-ranks device time (strong scaling).
 --impl reference: the reference's own CPU engine (oracle/_ref, built from
 /root/reference) on the same workload, bounded samples, rank 0 only.
 """
@@ -254,29 +255,47 @@ def run_ours(args, world, rank, local):
         raise SystemExit("no CUDA device: the B200 data plane has no CPU fallback")
     torch.cuda.set_device(local)
     aut = sw.from_spec(args.workload)
+    nvlink = []
+    if world > 1:
+        # ONE partitioned solve over the N GPUs (hash ownership):
+        # NCCL communicator, per-level all-to-all to the owners, all-gathers
+        # for containment, all-reduced statistics, DFS shares + MIN.
+        from paper_2207_05495_b200 import distributed
+        comm = distributed.make_comm("nccl")
+
+        def solve(**kw):
+            r, sent = distributed.solve_exact_partitioned(aut, comm, device=local, **kw)
+            nvlink.append(sent)
+            return r
+    else:
+        def solve(**kw):
+            return sw.solve_exact(aut, device=local, **kw)
     # Heuristic bound R once (the reference computes the same R, bit-identical).
-    R = sw.solve_exact(aut, device=local).upper_bound
+    R = solve().upper_bound
     W = (aut.n + 63) // 64
     exp_bytes_per_child = 8 * W / aut.k + 8 * W + 4  # parent/k + child + card
 
     for _ in range(max(3, args.warmup)):
-        sw.solve_exact(aut, upper_bound=R, device=local, timing=True)
+        solve(upper_bound=R, timing=True)
 
     flush_l2(local)
     barrier(world)
     torch.cuda.synchronize()
     results = []
+    nvlink.clear()
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(local)  # between timed steps: L2 flushed (device time excludes the flush)
-            results.append(sw.solve_exact(aut, upper_bound=R, device=local, timing=True))
+            results.append(solve(upper_bound=R, timing=True))
     torch.cuda.synchronize()
     barrier(world)
     dev_s = sum(r.engine_device_ms for r in results) / 1e3
     dev_s_max = max_over_ranks(world, dev_s)
     expansions = results[0].expansions
-    total_units = sum_over_ranks(world, float(sum(r.expansions for r in results)))
+    # the partitioned solve reports global counts on every rank: the job's units
+    total_units = float(sum(r.expansions for r in results))
     value = total_units / dev_s_max
+    nvlink_sent = sum_over_ranks(world, float(sum(nvlink))) / max(1, args.steps) if world > 1 else 0
     launches = sum(r.kernel_launches for r in results)
     exp_children = sum(r.expansions for r in results)
     exp_ms = sum(r.expand_kernel_ms for r in results)
@@ -286,14 +305,15 @@ def run_ours(args, world, rank, local):
     # e2e: public call, host transition table in, threshold + word out, heuristic included.
     e2e = []
     for _ in range(2):  # untimed warm-up of the public path (first use of the heuristic kernels)
-        sw.solve_exact(aut, device=local, track_word=True)
+        solve(track_word=True)
     for _ in range(max(1, min(args.steps, 3))):
         flush_l2(local)
+        barrier(world)
         t = time.perf_counter()
-        r = sw.solve_exact(aut, device=local, track_word=True)
+        r = solve(track_word=True)
         e2e.append((time.perf_counter() - t, r))
     e2e_s = max_over_ranks(world, sum(x[0] for x in e2e))
-    e2e_units = sum_over_ranks(world, float(sum(x[1].expansions for x in e2e)))
+    e2e_units = float(sum(x[1].expansions for x in e2e))
     last = e2e[-1][1]
     assert last.word is not None and len(last.word) == last.threshold and sw.is_reset_word(aut, last.word)
 
@@ -319,7 +339,7 @@ def run_ours(args, world, rank, local):
     # Containment as work rather than bytes: one untimed solve with
     # the traversal counters on; node visits + range-scan pair tests per second of
     # the timed traversal, against the INT32 logic ceiling.
-    cs = sw.solve_exact(aut, upper_bound=R, device=local, contain_stats=True)
+    cs = solve(upper_bound=R, contain_stats=True)
     cont_ms_solve = cont_ms / len(results)
     logic_rate = ((cs.contain_visits + cs.contain_pairs) / (cont_ms_solve / 1e3)
                   if cont_ms_solve > 0 else None)
@@ -331,7 +351,7 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": dev_s_max * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (SplitMix64 random automaton, automaton.hpp:159-164)",
         "config": arm_config(args.workload, aut.n, aut.k, R, world, results[0].threshold,
                              expansions),
@@ -390,9 +410,11 @@ def run_ours(args, world, rank, local):
             line["e2e"]["vs_reference_time_to_threshold"] = (
                 line["cpu_baseline"]["time_to_threshold_s"] / line["e2e"]["time_to_threshold_s"])
     if world > 1:
+        line["nvlink_bytes_per_solve"] = nvlink_sent
+        line["nvlink_gbs"] = nvlink_sent / (dev_s_max / args.steps) / 1e9 if dev_s_max else None
         try:
             line["exchange"] = exchange_probe(aut.n, world, rank)
-        except Exception as e:  # the replica numbers above stand on their own
+        except Exception as e:  # the partitioned-solve numbers above stand on their own
             line["exchange"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     line["clocks"] = clocks.summary()
     if rank == 0:
@@ -436,7 +458,8 @@ def arm_config(workload, n, k, R, world, threshold=None, expansions=None):
                         "bit-identical to the reference's)",
             "n": n, "k": k, "threshold": threshold, "expansions_per_solve": expansions,
             "l2": "flushed between timed steps (512 MiB write; device time excludes it)",
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+            "parallelism": (f"one solve partitioned over {world} GPUs by hash ownership (NCCL)"
+                            if world > 1 else "single GPU")}
 
 
 def run_reference(args, world, rank):
@@ -464,7 +487,7 @@ def run_reference(args, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (SplitMix64 random automaton)",
         "config": dict(arm_config(args.workload, n, k, ub, world),
                        reference_step=f"PREFIX: the first {its} iterations of the solve per step "

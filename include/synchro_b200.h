@@ -80,6 +80,10 @@ typedef struct sw_solve_options {
   double beam_cost_fraction;   /* 0.05 */
   double reduction_of_reduction; /* <= 0: unset (1/k) */
   uint64_t stop_after_iterations; /* analysis: stop after this many iterations (0: never) */
+  int32_t dfs_reference_order; /* 1 (default): DFS slices in the reference's exact order
+                                  (per-level sizes identical); 0: (card desc, lex) slices
+                                  (same threshold, no host-side order replay) */
+  int32_t pad_;
 } sw_solve_options;
 
 /* SolveResult (bibfs_engine.hpp:50-59) + expansion counters and timings. */

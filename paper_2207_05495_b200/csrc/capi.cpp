@@ -98,6 +98,7 @@ SolveOptions to_options(const sw_solve_options* o) {
   s.tuning.beam_cost_fraction = o->beam_cost_fraction;
   if (o->reduction_of_reduction > 0) s.tuning.cost.dfs_reduction_of_reduction = o->reduction_of_reduction;
   s.stop_after_iterations = o->stop_after_iterations;
+  s.dfs_reference_order = o->dfs_reference_order != 0;
   s.device = o->device;
   s.timing = o->timing != 0;
   s.contain_stats = o->contain_stats != 0;
@@ -147,6 +148,7 @@ SW_EXPORT void sw_default_options(sw_solve_options* o) {
   o->beam_cost_fraction = 0.05;
   o->reduction_of_reduction = 0.0;
   o->stop_after_iterations = 0;
+  o->dfs_reference_order = 1;
 }
 
 SW_EXPORT int sw_random_automaton(uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta_out) {
@@ -527,7 +529,7 @@ SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
       c.free(dkeep);
       return;
     }
-    if (dev::use_trie_index()) {
+    if (dev::use_trie_for_marks()) {
       const dev::TrieQueryIndex t = dev::build_trie_index(c, a, dev::kTrieLeafKeys);
       uint8_t* dkeep = static_cast<uint8_t*>(c.alloc(std::max<size_t>(b_count, 1)));
       dev::trie_superset_flags(c, t, b, mode == 1, dkeep);

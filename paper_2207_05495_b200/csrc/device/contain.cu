@@ -927,7 +927,7 @@ size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper) {
     brute_keep_flags(c, A, b, /*super=*/false, proper, keep);
     return before - compact_flags(c, b, keep, nullptr);
   }
-  if (use_trie_index()) {
+  if (use_trie_for_marks()) {
     const size_t before = b.size();
     const TrieQueryIndex t = build_trie_index(c, A, kTrieLeafKeys);
     auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
@@ -946,7 +946,7 @@ size_t self_reduce_minimal(Context& c, DList& l) {
     brute_keep_flags(c, l, l, /*super=*/false, /*proper=*/true, keep);
     return before - compact_flags(c, l, keep, nullptr);
   }
-  if (use_trie_index()) return trie_self_reduce_minimal(c, l);
+  if (use_trie_for_marks()) return trie_self_reduce_minimal(c, l);
   const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
   // The queries are the keys themselves: query with the index's own sorted,
   // relabelled rows (best locality), then map the flags back to l's order.

@@ -250,6 +250,8 @@ DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool
 void merge_sorted(Context& c, DList& h, const DList& add);
 // l := rows perm[0], perm[1], ... of l (perm: device array of l.size() indices).
 void gather_rows(Context& c, DList& l, const u32* perm);
+// tags[i] += add (a partitioned level's parent indices made global).
+void add_to_tags(Context& c, DList& l, u64 add);
 u64 read_tag(Context& c, const DList& l, size_t i);
 std::vector<u64> read_tags(Context& c, const DList& l);
 
@@ -323,7 +325,8 @@ void trie_superset_flags(Context& c, const TrieQueryIndex& t, const DList& b, bo
 size_t trie_self_reduce_minimal(Context& c, DList& l);
 // Which containment index the list paths use: the reference's trie shape
 // (default) or the relabelled radix tree (SYNCHRO_INDEX=radix, A/B only).
-bool use_trie_index();
+bool use_trie_index();       // existence queries
+bool use_trie_for_marks();   // marking (self-reduction, history)
 constexpr u32 kTrieLeafKeys = 16;
 
 // ---- microbenchmarks (microbench.cu): avg CUDA-event ms per call on `count`

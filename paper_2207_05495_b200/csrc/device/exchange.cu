@@ -44,9 +44,11 @@ __global__ void owner_count_kernel(const u64* __restrict__ words, u64 N, u32 W, 
 }
 
 __global__ void owner_scatter_kernel(const u64* __restrict__ words, const u32* __restrict__ cards,
-                                     u64 N, u32 W, const u32* __restrict__ owner,
+                                     const u64* __restrict__ tags, u64 N, u32 W,
+                                     const u32* __restrict__ owner,
                                      unsigned long long* __restrict__ cursor,
-                                     u64* __restrict__ ow, u32* __restrict__ oc) {
+                                     u64* __restrict__ ow, u32* __restrict__ oc,
+                                     u64* __restrict__ ot) {
   const u32 lane = threadIdx.x & 31;
   const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
   for (u64 i0 = blockIdx.x * static_cast<u64>(blockDim.x) + (threadIdx.x & ~31u); i0 < N; i0 += stride) {
@@ -63,6 +65,7 @@ __global__ void owner_scatter_kernel(const u64* __restrict__ words, const u32* _
       const u64 dst = base + __popc(peers & ((1u << lane) - 1));
       for (u32 w = 0; w < W; ++w) ow[dst * W + w] = words[i * W + w];
       oc[dst] = cards[i];
+      if (tags) ot[dst] = tags[i];
     }
   }
 }
@@ -84,9 +87,10 @@ std::vector<u64> owner_partition(Context& c, DList& l, u32 nranks) {
   std::vector<u64> start(nranks, 0);
   for (u32 r = 1; r < nranks; ++r) start[r] = start[r - 1] + counts[r - 1];
   c.memcpy_h2d(cnt + nranks, start.data(), static_cast<size_t>(nranks) * 8);
-  DList out(&c, N, false);
-  owner_scatter_kernel<<<grid_for(N, 256), 256, 0, s>>>(l.words, l.cards, N, W, owner, cnt + nranks,
-                                                        out.words, out.cards);
+  DList out(&c, N, l.tagged());
+  owner_scatter_kernel<<<grid_for(N, 256), 256, 0, s>>>(
+      l.words, l.cards, l.tagged() ? l.tags : nullptr, N, W, owner, cnt + nranks, out.words,
+      out.cards, l.tagged() ? out.tags : nullptr);
   SW_CHECK_LAUNCH();
   out.set_size(N);
   c.free(owner);

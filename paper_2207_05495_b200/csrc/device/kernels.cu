@@ -22,14 +22,25 @@ namespace synchro::dev {
 
 constexpr int kSliceWarps = 4;
 constexpr size_t kStageSmemLimit = 200 * 1024;
+// Image as a gather over the CSR of delta^-1 (out[t] = OR of the slices of
+// t's sources, divergent only in the in-degree) instead of shared-memory
+// atomicOr scatters into per-warp output slices.
+#ifndef SW_IMAGE_GATHER
+#define SW_IMAGE_GATHER 1
+#endif
+constexpr bool kImageGather = SW_IMAGE_GATHER != 0;
 
-// Shared memory of the sliced kernel: per warp 64W input slices + 64W output
-// slices, and (STAGED) a 64·k·W-word child block + 64·k cards; then the table.
+// Shared memory of the sliced kernel: per warp 64W input slices (+ 64W output
+// slices for the scatter image), and (STAGED) a 64·k·W-word child block +
+// 64·k cards; then the table (u16 delta, or the CSR of delta^-1).
 template <int W>
 static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
-  size_t per_warp = (inverse ? 1 : 2) * 64 * W * sizeof(u64);  // preimage: no output slices
+  const bool out_slices = !inverse && !kImageGather;
+  size_t per_warp = (out_slices ? 2 : 1) * 64 * W * sizeof(u64);
   if (staged) per_warp += static_cast<size_t>(64) * k * (W * sizeof(u64) + sizeof(u32));
-  return kSliceWarps * per_warp + ((static_cast<size_t>(k) * n * 2 + 15) & ~size_t{15});
+  const size_t kn = static_cast<size_t>(k) * n;
+  const size_t table = (!inverse && kImageGather) ? (kn + 1) * 4 + kn * 2 : kn * 2;
+  return kSliceWarps * per_warp + ((table + 15) & ~size_t{15});
 }
 
 // STAGED: the warp's 64 parents arrive as one contiguous block (coalesced
@@ -48,8 +59,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // [warps][64W] input slices, [warps][64W] output slices (image),
   // (STAGED) [warps][64kW] child block, [warps][64k] cards; table u16[k][n]
+  constexpr bool GATHER = !INV && kImageGather;
   u64* s_slices = reinterpret_cast<u64*>(smem);
-  unsigned char* p = smem + (INV ? 1 : 2) * kSliceWarps * 64 * W * sizeof(u64);
+  unsigned char* p = smem + ((INV || GATHER) ? 1 : 2) * kSliceWarps * 64 * W * sizeof(u64);
   u64* stage = nullptr;
   u32* scard = nullptr;
   if (STAGED) {
@@ -59,10 +71,17 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     p += static_cast<size_t>(kSliceWarps) * 64 * k * sizeof(u32);
   }
   uint16_t* s_tab = reinterpret_cast<uint16_t*>(p);
-  for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
+  u32* s_off = reinterpret_cast<u32*>(p);  // GATHER: CSR offsets, then sources
+  uint16_t* s_src = reinterpret_cast<uint16_t*>(s_off + kn + 1);
+  if (GATHER) {
+    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_src[i] = g_src[i];
+  } else {
+    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
+  }
   __syncthreads();
   u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
-  u64* so = INV ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
+  u64* so = (INV || GATHER) ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
   const u64 batches = (count + 63) / 64;
   for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
@@ -94,7 +113,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     for (u32 a = 0; a < k; ++a) {
       const u32 base = a * n;
       u32 card0 = 0, card1 = 0;
-      if (!INV) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
+      if (!INV && !GATHER) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
 #pragma unroll
         for (int i = 0; i < 2 * W; ++i) so[32 * i + lane] = 0;
         __syncwarp();
@@ -113,10 +132,17 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const u32 p = 64 * w + 32 * h + lane;
-          if (INV)
+          if (INV) {
             s[h] = p < n ? sl[s_tab[base + p]] : 0;  // preimage: pure gather
-          else
+          } else if (GATHER) {  // image: OR of the slices of p's sources under letter a
+            u64 acc = 0;
+            if (p < n)
+              for (u32 e = s_off[base + p], end = s_off[base + p + 1]; e < end; ++e)
+                acc |= sl[s_src[e]];
+            s[h] = acc;
+          } else {
             s[h] = so[p];
+          }
         }
         u64 r0, r1;
         transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
@@ -456,6 +482,19 @@ size_t compact_flags(Context& c, DList& l, const uint8_t* keep, const u32* perm)
 }
 
 void gather_rows(Context& c, DList& l, const u32* perm) { compact_flags(c, l, nullptr, perm); }
+
+__global__ void add_to_tags_kernel(u64* __restrict__ tags, u64 count, u64 add) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    tags[i] += add;
+}
+
+void add_to_tags(Context& c, DList& l, u64 add) {
+  if (!l.tagged() || l.empty() || add == 0) return;
+  add_to_tags_kernel<<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(l.tags, l.size(), add);
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches++;
+}
 
 size_t compact_unique(Context& c, DList& l, const u32* perm) {
   size_t r = 0;

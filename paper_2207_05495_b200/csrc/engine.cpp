@@ -8,6 +8,7 @@
 #include <set>
 #include <sstream>
 
+#include "comm.hpp"
 #include "device/dev.hpp"
 #include "meet_order.hpp"
 #include "progress.hpp"
@@ -30,14 +31,23 @@ GpuBibfs::GpuBibfs(const Automaton& aut, u64 upper_bound, const SolveOptions& op
       n_(aut.state_count()),
       k_(aut.alphabet_size()),
       R_(upper_bound) {
-  lbfs_ = std::make_unique<DList>(dev::make_universe(ctx_, opt_.track_word));
+  const bool lead = !dist() || opt_.comm->rank() == 0;
+  // Partitioned solve: rank 0 creates the frontier lists, the exchange hands
+  // every set to its owner; the histories are replicated.
+  lbfs_ = std::make_unique<DList>(lead ? dev::make_universe(ctx_, opt_.track_word)
+                                       : DList(&ctx_, 0, opt_.track_word));
   hbfs_ = std::make_unique<DList>(dev::make_universe(ctx_, false));
-  libfs_ = std::make_unique<DList>(dev::make_singletons(ctx_, opt_.track_word));
+  libfs_ = std::make_unique<DList>(lead ? dev::make_singletons(ctx_, opt_.track_word)
+                                        : DList(&ctx_, 0, opt_.track_word));
   hibfs_c_ = std::make_unique<DList>(dev::make_singletons(ctx_, false));
   dev::complement(ctx_, *hibfs_c_);
-  refresh(*lbfs_, lbfs_i_);
+  if (dist()) {
+    exchange(*lbfs_);
+    exchange(*libfs_);
+  }
+  refresh_part(*lbfs_, lbfs_i_);
   refresh(*hbfs_, hbfs_i_);
-  refresh(*libfs_, libfs_i_);
+  refresh_part(*libfs_, libfs_i_);
   refresh(*hibfs_c_, hibfs_i_);
   ledger_.charge_or_throw(list_footprint(n_, lbfs_i_.size) + list_footprint(n_, libfs_i_.size) +
                           list_footprint(n_, hbfs_i_.size) + list_footprint(n_, hibfs_i_.size));
@@ -56,6 +66,87 @@ void GpuBibfs::refresh(const DList& l, Info& info) {
   info.sum_cards = st.sum_cards;
   info.min_card = st.min_card;
   info.max_card = st.max_card;
+}
+
+// -------------------------------------------------- partitioned solve (comm.hpp)
+// Statistics of a partitioned list over all ranks: the cost model, the
+// ledger and the trace see the global integers, so every rank takes the
+// single-GPU solve's steps.
+void GpuBibfs::refresh_part(const DList& l, Info& info) {
+  refresh(l, info);
+  if (!dist()) return;
+  u64 v[2] = {info.size, info.sum_cards};
+  opt_.comm->all_reduce(ctx_, v, 2, ReduceOp::Sum);
+  u64 mn = info.size ? info.min_card : n_, mx = info.size ? info.max_card : 0;
+  opt_.comm->all_reduce(ctx_, &mn, 1, ReduceOp::Min);
+  opt_.comm->all_reduce(ctx_, &mx, 1, ReduceOp::Max);
+  info.size = v[0];
+  info.sum_cards = v[1];
+  info.min_card = static_cast<u32>(mn);
+  info.max_card = static_cast<u32>(mx);
+}
+
+u64 GpuBibfs::allsum(u64 v) {
+  if (dist()) opt_.comm->all_reduce(ctx_, &v, 1, ReduceOp::Sum);
+  return v;
+}
+
+// Hash ownership: every row travels to rank h(row) mod nranks
+// (exchange.cu owner_partition + one all-to-all per array).
+void GpuBibfs::exchange(DList& l) {
+  Comm& cm = *opt_.comm;
+  const std::vector<u64> send = dev::owner_partition(ctx_, l, static_cast<u32>(cm.size()));
+  const std::vector<u64> recv = cm.all_to_all_counts(ctx_, send);
+  u64 total = 0;
+  for (u64 r : recv) total += r;
+  DList out(&ctx_, total, l.tagged());
+  const auto scaled = [](const std::vector<u64>& v, u64 b) {
+    std::vector<u64> o(v.size());
+    for (size_t i = 0; i < v.size(); ++i) o[i] = v[i] * b;
+    return o;
+  };
+  const u64 row = static_cast<u64>(ctx_.W()) * 8;
+  cm.all_to_allv(ctx_, l.words, scaled(send, row), out.words, scaled(recv, row));
+  cm.all_to_allv(ctx_, l.cards, scaled(send, 4), out.cards, scaled(recv, 4));
+  if (l.tagged()) cm.all_to_allv(ctx_, l.tags, scaled(send, 8), out.tags, scaled(recv, 8));
+  out.set_size(total);
+  l = std::move(out);
+}
+
+// The whole partitioned list on every rank, rank by rank (containment is not
+// hash-local: a subset of an owned set may live on any rank).
+DList GpuBibfs::gather(const DList& l, bool tags) {
+  Comm& cm = *opt_.comm;
+  const std::vector<u64> sizes = cm.all_gather_u64(ctx_, l.size());
+  u64 total = 0;
+  for (u64 x : sizes) total += x;
+  const bool tg = tags && l.tagged();
+  DList out(&ctx_, total, tg);
+  const auto scaled = [&](u64 b) {
+    std::vector<u64> o(sizes.size());
+    for (size_t i = 0; i < sizes.size(); ++i) o[i] = sizes[i] * b;
+    return o;
+  };
+  const u64 row = static_cast<u64>(ctx_.W()) * 8;
+  cm.all_gather_v(ctx_, l.words, l.size() * row, out.words, scaled(row));
+  cm.all_gather_v(ctx_, l.cards, l.size() * 4, out.cards, scaled(4));
+  if (tg) cm.all_gather_v(ctx_, l.tags, l.size() * 8, out.tags, scaled(8));
+  out.set_size(total);
+  return out;
+}
+
+// Global index of this rank's first row of a partitioned list (rank order).
+u64 GpuBibfs::rank_offset(const DList& l) {
+  const std::vector<u64> sizes = opt_.comm->all_gather_u64(ctx_, l.size());
+  u64 off = 0;
+  for (int r = 0; r < opt_.comm->rank(); ++r) off += sizes[r];
+  return off;
+}
+
+// Level tags in the global (rank-concatenated) order of a partitioned level.
+std::vector<u64> GpuBibfs::level_tags(const DList& l) {
+  if (!dist()) return dev::read_tags(ctx_, l);
+  return dev::read_tags(ctx_, gather(l, true));
 }
 
 // set_list.hpp:171-174
@@ -203,24 +294,43 @@ void GpuBibfs::bfs_step(bool with_history) {
     ledger_.release(before - list_footprint(n_, hbfs_i_.size));
   }
   charge_layer(lbfs_i_.size);
-  DList next(&ctx_, lbfs_i_.size * k_, opt_.track_word);
-  dev::expand(ctx_, *lbfs_, 0, lbfs_i_.size, /*inverse=*/false, next);
+  DList next(&ctx_, lbfs_->size() * k_, opt_.track_word);
+  dev::expand(ctx_, *lbfs_, 0, lbfs_->size(), /*inverse=*/false, next);
   Rollback rb{ledger_, charged_layer_};
-  const size_t generated = next.size();
+  if (dist()) {  // global parent indices, then every child to its owner
+    if (opt_.track_word) dev::add_to_tags(ctx_, next, rank_offset(*lbfs_) << 16);
+    exchange(next);
+  }
+  const size_t generated = lbfs_i_.size * k_;
   // Set-semantics dedupe (hash; same survivors as the reference's stable lex
   // sort + unique).  L_BFS needs no lex order: every consumer either sorts its
   // own relabelled copy (containment index) or is order-free (stats, ledger).
-  const double r_dupl = generated ? ratio(dev::hash_dedupe(ctx_, next, /*first_occurrence=*/false), generated) : 0.0;
-  const size_t after_dupl = next.size();
-  const double r_self = ratio(dev::self_reduce_minimal(ctx_, next), after_dupl);
-  double r_hist = 0.0;
-  if (with_history) {
-    const size_t before = next.size();
-    const size_t removed = dev::remove_supersets_of(ctx_, *hbfs_, next, /*proper=*/false);
-    r_hist = ratio(removed, before);
+  // Partitioned: equal sets share an owner, so the owner's dedupe is exact.
+  const double r_dupl =
+      generated ? ratio(allsum(dev::hash_dedupe(ctx_, next, /*first_occurrence=*/false)), generated)
+                : 0.0;
+  const size_t after_dupl = allsum(next.size());
+  size_t removed_self;
+  if (dist()) {  // owned sets against the whole deduplicated layer
+    const DList layer = gather(next, false);
+    removed_self = dev::remove_supersets_of(ctx_, layer, next, /*proper=*/true);
+  } else {
+    removed_self = dev::self_reduce_minimal(ctx_, next);
   }
-  shrink_charge(next.size());
-  if (with_history) merge_history(*hbfs_, hbfs_i_, next);
+  const double r_self = ratio(allsum(removed_self), after_dupl);
+  double r_hist = 0.0;
+  if (with_history) {  // the history is replicated
+    const size_t before = allsum(next.size());
+    const size_t removed = dev::remove_supersets_of(ctx_, *hbfs_, next, /*proper=*/false);
+    r_hist = ratio(allsum(removed), before);
+  }
+  shrink_charge(allsum(next.size()));
+  if (with_history) {
+    if (dist())
+      merge_history(*hbfs_, hbfs_i_, gather(next, false));
+    else
+      merge_history(*hbfs_, hbfs_i_, next);
+  }
   // commit (bibfs_engine.hpp:375-379)
   ledger_.release(list_footprint(n_, lbfs_i_.size));
   if (lbfs_met_ && lbfs_i_.size >= opt_.tuning.min_brute)  // its meet permuted L_IBFS
@@ -229,10 +339,10 @@ void GpuBibfs::bfs_step(bool with_history) {
   *lbfs_ = std::move(next);
   lbfs_index_.reset();
   lbfs_trie_.reset();
-  refresh(*lbfs_, lbfs_i_);
+  refresh_part(*lbfs_, lbfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
-  if (opt_.track_word) bfs_levels_.push_back(dev::read_tags(ctx_, *lbfs_));
+  if (opt_.track_word) bfs_levels_.push_back(level_tags(*lbfs_));
   ratio_bfs_[0] = 0.5 * ratio_bfs_[0] + 0.5 * r_dupl;
   ratio_bfs_[1] = 0.5 * ratio_bfs_[1] + 0.5 * r_self;
   if (with_history) ratio_bfs_[2] = 0.5 * ratio_bfs_[2] + 0.5 * r_hist;
@@ -257,38 +367,54 @@ void GpuBibfs::ibfs_step(bool with_history) {
     ledger_.release(before - list_footprint(n_, hibfs_i_.size));
   }
   charge_layer(libfs_i_.size);
-  DList next(&ctx_, libfs_i_.size * k_, opt_.track_word);
-  dev::expand(ctx_, *libfs_, 0, libfs_i_.size, /*inverse=*/true, next);
+  DList next(&ctx_, libfs_->size() * k_, opt_.track_word);
+  dev::expand(ctx_, *libfs_, 0, libfs_->size(), /*inverse=*/true, next);
   Rollback rb{ledger_, charged_layer_};
   dev::complement(ctx_, next);
-  const size_t generated = next.size();
-  const double r_dupl = generated ? ratio(dev::lex_sort_dedupe(ctx_, next), generated) : 0.0;
-  const size_t after_dupl = next.size();
+  if (dist()) {
+    if (opt_.track_word) dev::add_to_tags(ctx_, next, rank_offset(*libfs_) << 16);
+    exchange(next);
+  }
+  const size_t generated = libfs_i_.size * k_;
+  const double r_dupl = generated ? ratio(allsum(dev::lex_sort_dedupe(ctx_, next)), generated) : 0.0;
+  const size_t after_dupl = allsum(next.size());
   // The reductions of the reference run on complements (minimal sets there);
   // on plain sets they are superset queries — done by the bucketed superset
   // join, which keeps the complement-lex order of `next`.
   dev::complement(ctx_, next);
-  const double r_self = ratio(dev::self_reduce_maximal(ctx_, next), after_dupl);
+  size_t removed_self;
+  if (dist()) {
+    const DList layer = gather(next, false);
+    removed_self = dev::remove_subsets_of(ctx_, layer, next, /*proper=*/true);
+  } else {
+    removed_self = dev::self_reduce_maximal(ctx_, next);
+  }
+  const double r_self = ratio(allsum(removed_self), after_dupl);
   double r_hist = 0.0;
   if (with_history) {
-    const size_t before = next.size();
+    const size_t before = allsum(next.size());
     DList h_plain = dev::copy_list(ctx_, *hibfs_c_, false);
     dev::complement(ctx_, h_plain);
     const size_t removed = dev::remove_subsets_of(ctx_, h_plain, next, /*proper=*/false);
-    r_hist = ratio(removed, before);
+    r_hist = ratio(allsum(removed), before);
   }
   dev::complement(ctx_, next);
-  shrink_charge(next.size());
-  if (with_history) merge_history(*hibfs_c_, hibfs_i_, next);
+  shrink_charge(allsum(next.size()));
+  if (with_history) {
+    if (dist())
+      merge_history(*hibfs_c_, hibfs_i_, gather(next, false));
+    else
+      merge_history(*hibfs_c_, hibfs_i_, next);
+  }
   dev::complement(ctx_, next);
   ledger_.release(list_footprint(n_, libfs_i_.size));
   *libfs_ = std::move(next);
   met_lists_.clear();  // a fresh L_IBFS in complement-lex order
   lbfs_met_ = false;
-  refresh(*libfs_, libfs_i_);
+  refresh_part(*libfs_, libfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
-  if (opt_.track_word) ibfs_levels_.push_back(dev::read_tags(ctx_, *libfs_));
+  if (opt_.track_word) ibfs_levels_.push_back(level_tags(*libfs_));
   ratio_ibfs_[0] = 0.5 * ratio_ibfs_[0] + 0.5 * r_dupl;
   ratio_ibfs_[1] = 0.5 * ratio_ibfs_[1] + 0.5 * r_self;
   if (with_history) ratio_ibfs_[2] = 0.5 * ratio_ibfs_[2] + 0.5 * r_hist;
@@ -308,13 +434,51 @@ void GpuBibfs::perform(StepKind kind) {
 // Meet: is some X in L_BFS a subset of some Y in L_IBFS?
 // Small lists: one all-pairs launch instead of building the index.
 bool GpuBibfs::meet() {
+  // No L_BFS set can lie inside a smaller L_IBFS set: the reference's per-pair
+  // card filter (subset_algebra.hpp:66) decides the whole check — e.g. every
+  // meet against the initial singletons — without building an index.
+  const bool hopeless = lbfs_i_.min_card > libfs_i_.max_card;
+  if (dist()) {
+    if (hopeless) return false;  // owned L_BFS sets against the whole L_IBFS, any rank's hit counts
+    const DList ibfs = gather(*libfs_, false);
+    bool met = false;
+    if (!lbfs_->empty() && !ibfs.empty())
+      met = dev::brute_fits(lbfs_->size(), ibfs.size())
+                ? dev::brute_exists_subset(ctx_, *lbfs_, ibfs, nullptr)
+                : exists_in_bfs(ibfs, nullptr);
+    return allsum(met ? 1 : 0) > 0;
+  }
   lbfs_met_ = !opt_.track_word;  // meet_check permutes L_IBFS (subset_algebra.hpp:201-210)
+  if (hopeless) return false;
   if (dev::brute_fits(lbfs_->size(), libfs_->size()))
     return dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, nullptr);
   return exists_in_bfs(*libfs_, nullptr);
 }
 
 bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
+  if (lbfs_i_.min_card > libfs_i_.max_card) return false;  // as meet()
+  if (dist()) {  // the lowest rank with a hit reports (global L_BFS index, L_IBFS tag)
+    const DList ibfs = gather(*libfs_, true);
+    dev::Witness w;
+    bool met = false;
+    if (!lbfs_->empty() && !ibfs.empty())
+      met = dev::brute_fits(lbfs_->size(), ibfs.size())
+                ? dev::brute_exists_subset(ctx_, *lbfs_, ibfs, &w)
+                : exists_in_bfs(ibfs, &w);
+    const u64 off = rank_offset(*lbfs_);
+    u64 winner = met ? static_cast<u64>(opt_.comm->rank()) : static_cast<u64>(opt_.comm->size());
+    opt_.comm->all_reduce(ctx_, &winner, 1, ReduceOp::Min);
+    if (winner == static_cast<u64>(opt_.comm->size())) return false;
+    u64 v[2] = {0, 0};
+    if (winner == static_cast<u64>(opt_.comm->rank())) {
+      v[0] = off + w.a_index;
+      v[1] = dev::read_tag(ctx_, ibfs, w.b_index);
+    }
+    opt_.comm->all_reduce(ctx_, v, 2, ReduceOp::Sum);
+    *bfs_index_out = static_cast<size_t>(v[0]);
+    *ibfs_tag = v[1];
+    return true;
+  }
   dev::Witness w;
   const bool met = dev::brute_fits(lbfs_->size(), libfs_->size())
                        ? dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, &w)
@@ -383,9 +547,9 @@ class DfsRunner {
   using Query = std::function<bool(const DList&, dev::Witness*)>;
   DfsRunner(dev::Context& c, const DList& lbfs, Query query, MemoryLedger& ledger,
             const EngineTuning& t, const Deadline& deadline, bool tracking,
-            std::vector<std::array<u64, 5>>* log)
+            std::vector<std::array<u64, 5>>* log, bool reference_order)
       : c_(c), lbfs_(lbfs), query_(std::move(query)), ledger_(ledger), t_(t), deadline_(deadline),
-        tracking_(tracking), log_(log) {}
+        tracking_(tracking), log_(log), reference_order_(reference_order) {}
 
   // Shard s of c explores the subtrees of initial[i] for i ≡ s (mod c) only
   // (c = 1: everything).  Interleaved rather than contiguous shares: the work
@@ -471,7 +635,7 @@ class DfsRunner {
     const size_t cap = slice_cap(r);
     if (next.size() > cap) {  // slices follow the order the trie queries left
       dev::sort_card_desc_lex(c_, next);
-      replay_query_order(next, cap);
+      if (reference_order_) replay_query_order(next, cap);
     }
     const Frame frame{parent, &next};
     for (size_t plo = 0; plo < next.size(); plo += cap) {
@@ -486,6 +650,7 @@ class DfsRunner {
   // Only groups that straddle a slice boundary change which sets share a
   // slice; their order is replayed on the host (meet_order.cpp).
   void replay_query_order(DList& level, size_t cap) {
+    const auto t0 = std::chrono::steady_clock::now();
     const size_t N = level.size();
     std::vector<u32> cards(N);
     dev::download(c_, level, nullptr, cards.data(), nullptr);
@@ -518,6 +683,11 @@ class DfsRunner {
     c_.memcpy_h2d(d, perm.data(), N * 4);
     dev::gather_rows(c_, level, d);
     c_.free(d);
+    size_t gq = 0;
+    for (const auto& g : groups) gq += g.second - g.first;
+    SYNCHRO_PROGRESS("  dfs slice order replay: |level|=%zu groups=%zu queries=%zu %.3f s", N,
+                     groups.size(), gq,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
   }
 
   void record_find(const dev::Witness& w, const DList& level, const Frame* parent) {
@@ -544,6 +714,7 @@ class DfsRunner {
   const Deadline& deadline_;
   bool tracking_;
   std::vector<std::array<u64, 5>>* log_;
+  bool reference_order_;
   u64 bound_ = 0;
   size_t root_start_ = 0, root_stride_ = 1;
   DfsFind find_;
@@ -561,22 +732,71 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   drop_bfs_history();
   drop_ibfs_history();
   if (lbfs_i_.size == 0) return R_;
+  if (dist()) {  // the static structure over the WHOLE L_BFS on every rank; the
+                 // roots (L_IBFS) in global order, explored in interleaved shares
+    *lbfs_ = gather(*lbfs_, false);
+    *libfs_ = gather(*libfs_, opt_.track_word);
+    lbfs_index_.reset();
+    lbfs_trie_.reset();
+  }
   const u64 nodes = dev::trie_node_count(ctx_, *lbfs_, opt_.tuning.min_leaf);
   const u64 trie_bytes = list_footprint(n_, lbfs_i_.size) + nodes * 24;
   ledger_.charge_or_throw(trie_bytes);
   ledger_.release(list_footprint(n_, lbfs_i_.size));
   // The top-level slices follow L_IBFS's order: reproduce the reference's
   // post-meet_check order when they will actually cut the list.
-  if (!opt_.track_word && r < R_ && libfs_i_.size > dfs_slice_cap(ledger_, n_, k_, R_, r - 1))
+  if (!dist() && opt_.dfs_reference_order && !opt_.track_word && r < R_ &&
+      libfs_i_.size > dfs_slice_cap(ledger_, n_, k_, R_, r - 1))
     replay_meet_order();
   dump_list(ctx_, *lbfs_, "lbfs");
   dump_list(ctx_, *libfs_, "libfs");
   DfsRunner dfs(ctx_, *lbfs_, [this](const DList& b, dev::Witness* w) { return exists_in_bfs(b, w); },
-                ledger_, opt_.tuning, deadline_, opt_.track_word, log);
-  const u64 final_bound =
-      dfs.run(*libfs_, r, R_, opt_.dfs_shard_index, std::max<u32>(1, opt_.dfs_shard_count));
-  if (find) *find = dfs.find();
-  if (expansions) *expansions = dfs.expansions;
+                ledger_, opt_.tuning, deadline_, opt_.track_word, log,
+                opt_.dfs_reference_order);
+  const u32 shard = dist() ? static_cast<u32>(opt_.comm->rank()) : opt_.dfs_shard_index;
+  const u32 shards = dist() ? static_cast<u32>(opt_.comm->size())
+                            : std::max<u32>(1, opt_.dfs_shard_count);
+  u64 final_bound = dfs.run(*libfs_, r, R_, shard, shards);
+  DfsFind mine = dfs.find();
+  u64 exp = dfs.expansions;
+  if (dist()) {
+    // threshold = MIN over the shards; the lowest rank attaining it with a
+    // find hands its witness (trie index, root index, middle letters) to all
+    Comm& cm = *opt_.comm;
+    u64 best = final_bound;
+    cm.all_reduce(ctx_, &best, 1, ReduceOp::Min);
+    u64 winner = (mine.found && final_bound == best) ? static_cast<u64>(cm.rank())
+                                                     : static_cast<u64>(cm.size());
+    cm.all_reduce(ctx_, &winner, 1, ReduceOp::Min);
+    exp = allsum(exp);
+    if (winner < static_cast<u64>(cm.size())) {
+      std::vector<u64> pack;
+      if (winner == static_cast<u64>(cm.rank())) {
+        pack = {mine.trie_index, mine.root_index, mine.middle.size()};
+        for (u32 a : mine.middle) pack.push_back(a);
+      }
+      const std::vector<u64> len = cm.all_gather_u64(ctx_, pack.size());
+      u64* d = static_cast<u64*>(ctx_.alloc((len[winner] + 1) * 8));
+      u64* src = static_cast<u64*>(ctx_.alloc((pack.size() + 1) * 8));
+      ctx_.memcpy_h2d(src, pack.data(), pack.size() * 8);
+      std::vector<u64> rb(len.size());
+      for (size_t q = 0; q < len.size(); ++q) rb[q] = len[q] * 8;
+      cm.all_gather_v(ctx_, src, pack.size() * 8, d, rb);
+      std::vector<u64> got(len[winner]);
+      ctx_.memcpy_d2h(got.data(), d, got.size() * 8);
+      ctx_.free(d);
+      ctx_.free(src);
+      mine.found = true;
+      mine.trie_index = got[0];
+      mine.root_index = got[1];
+      mine.middle.assign(got.begin() + 3, got.begin() + 3 + static_cast<long>(got[2]));
+    } else {
+      mine.found = false;
+    }
+    final_bound = best;
+  }
+  if (find) *find = mine;
+  if (expansions) *expansions = exp;
   ledger_.release(trie_bytes);
   R_ = final_bound;
   return final_bound;

@@ -66,6 +66,12 @@ struct SolveOptions {
   // Analysis / prefix-parity hook: stop before iteration stop_after_iterations+1
   // (phase "stopped", threshold 0).  0 = run to the end.
   u64 stop_after_iterations = 0;
+  // DFS slices cut in the reference's exact order (the order meet_check and
+  // the trie queries leave the lists in, meet_order.cpp): per-level sizes
+  // bit-identical to the reference's.  false: slices of the (card desc, lex)
+  // order — the same threshold (every in-slice reduction keeps a dominating
+  // set), different DFS level sizes, no host replay.
+  bool dfs_reference_order = true;
   // Partitioned solve over several GPUs (comm.hpp; not owned).  nullptr: one GPU.
   Comm* comm = nullptr;
 };
@@ -146,6 +152,14 @@ class GpuBibfs {
   void drop_bfs_history();
   void drop_ibfs_history();
   void refresh(const dev::DList& l, Info& info);
+  // partitioned solve (opt_.comm): see engine.cpp
+  bool dist() const { return opt_.comm != nullptr; }
+  void refresh_part(const dev::DList& l, Info& info);
+  u64 allsum(u64 v);
+  void exchange(dev::DList& l);
+  dev::DList gather(const dev::DList& l, bool tags);
+  u64 rank_offset(const dev::DList& l);
+  std::vector<u64> level_tags(const dev::DList& l);
   double density(const Info& i) const;
   void charge_layer(size_t parents);
   void shrink_charge(size_t now_size);

@@ -91,3 +91,107 @@ def owner_exchange_dedupe(n: int, words, cards, group=None, partition=None, dedu
     bytes_sent = sum(c for r, c in enumerate(counts) if r != rank) * (8 * W + 4)
     ow, oc = dedupe(rw, rc)
     return ow, oc, bytes_sent
+
+
+# ------------------------------------------------------- partitioned solve
+class TorchCallbacks:
+    """Host-buffer collectives for sw_comm (SW_COMM_CALLBACK) over an
+    initialised torch.distributed process group on CPU tensors (gloo): the
+    engine stages its device buffers through host memory and calls these.
+    Pairwise send/recv for the variable-size exchanges (gloo has no
+    variable-size all-to-all), all_reduce for the statistics."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    @staticmethod
+    def _view(ptr, nbytes):
+        import ctypes
+        import numpy as np
+        import torch
+        if nbytes == 0:
+            return torch.empty(0, dtype=torch.uint8)
+        arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_uint8)), (nbytes,))
+        return torch.from_numpy(arr)
+
+    def _exchange(self, sends, recvs):
+        import torch.distributed as dist
+        ops = []
+        for r in range(self.world):
+            if r == self.rank:
+                if recvs[r].numel():
+                    recvs[r].copy_(sends[r])
+                continue
+            if sends[r].numel():
+                ops.append(dist.P2POp(dist.isend, sends[r], r, self.group))
+            if recvs[r].numel():
+                ops.append(dist.P2POp(dist.irecv, recvs[r], r, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def all_to_allv(self, user, send, send_bytes, recv, recv_bytes):
+        try:
+            sb = [int(send_bytes[r]) for r in range(self.world)]
+            rb = [int(recv_bytes[r]) for r in range(self.world)]
+            st, rt = self._view(send, sum(sb)), self._view(recv, sum(rb))
+            sends = list(st.split(sb)) if sum(sb) else [st[:0]] * self.world
+            recvs = list(rt.split(rb)) if sum(rb) else [rt[:0]] * self.world
+            self._exchange(sends, recvs)
+            return 0
+        except Exception:
+            return 1
+
+    def all_gather_v(self, user, send, nbytes, recv, recv_bytes):
+        try:
+            rb = [int(recv_bytes[r]) for r in range(self.world)]
+            st, rt = self._view(send, int(nbytes)), self._view(recv, sum(rb))
+            recvs = list(rt.split(rb)) if sum(rb) else [rt[:0]] * self.world
+            self._exchange([st] * self.world, recvs)
+            return 0
+        except Exception:
+            return 1
+
+    def all_reduce_u64(self, user, values, count, op):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        try:
+            arr = np.ctypeslib.as_array(values, (int(count),))
+            t = torch.from_numpy(arr.astype(np.int64))
+            dop = {0: dist.ReduceOp.SUM, 1: dist.ReduceOp.MIN, 2: dist.ReduceOp.MAX}[int(op)]
+            dist.all_reduce(t, op=dop, group=self.group)
+            arr[:] = t.numpy().astype(np.uint64)
+            return 0
+        except Exception:
+            return 1
+
+    def callbacks(self):
+        return (self.all_to_allv, self.all_gather_v, self.all_reduce_u64)
+
+
+def make_comm(kind: str = "callback", group=None):
+    """A native.Comm for this rank: "nccl" (rank 0 draws the unique id, one
+    all_gather_object shares it) or "callback" (TorchCallbacks over `group`)."""
+    import torch.distributed as dist
+    from . import native
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if kind == "nccl":
+        box = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return native.Comm(rank, world, nccl_id=box[0])
+    cb = TorchCallbacks(group)
+    comm = native.Comm(rank, world, callbacks=cb.callbacks())
+    comm._torch_callbacks = cb  # keep the bound methods alive
+    return comm
+
+
+def solve_exact_partitioned(aut, comm, trace_path=None, **opts):
+    """sw_solve_exact_dist on this rank (all ranks call it): the frontier lists
+    are partitioned by hash ownership, the per-level exchange is one
+    all-to-all, the trace and threshold are the single-GPU solve's."""
+    from . import native
+    return native.solve_exact_dist(aut, comm, trace_path=trace_path, **opts)

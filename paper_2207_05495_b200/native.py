@@ -75,7 +75,8 @@ class SolveOptions(C.Structure):
         ("contain_stats", C.c_int32), ("dfs_largest", C.c_uint64),
         ("history_growth", C.c_double), ("beam_initial", C.c_uint64),
         ("beam_cost_fraction", C.c_double), ("reduction_of_reduction", C.c_double),
-        ("stop_after_iterations", C.c_uint64),
+        ("stop_after_iterations", C.c_uint64), ("dfs_reference_order", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -90,6 +91,21 @@ class SolveResultC(C.Structure):
         ("phase", C.c_char * 16), ("engine_device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64), ("contain_kernel_ms", C.c_double), ("contain_bytes", C.c_uint64),
         ("contain_visits", C.c_uint64), ("contain_pairs", C.c_uint64),
+    ]
+
+
+A2A_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p,
+                     C.POINTER(C.c_uint64))
+AG_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64))
+AR_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64, C.c_int32)
+SW_COMM_NCCL, SW_COMM_CALLBACK = 1, 2
+
+
+class CommDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("pad", C.c_int32),
+        ("nccl_id", C.c_uint8 * 128), ("user", C.c_void_p), ("all_to_allv", A2A_CB),
+        ("all_gather_v", AG_CB), ("all_reduce_u64", AR_CB),
     ]
 
 
@@ -141,6 +157,12 @@ def load():
     L.sw_list_trie_exists.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
                                       C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
                                       C.POINTER(C.c_uint64)]
+    L.sw_nccl_unique_id.argtypes = [C.c_void_p]
+    L.sw_comm_create.argtypes = [C.POINTER(CommDesc), C.POINTER(C.c_void_p)]
+    L.sw_comm_destroy.argtypes = [C.c_void_p]
+    L.sw_solve_exact_dist.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(SolveOptions),
+                                      C.c_void_p, C.POINTER(SolveResultC), C.c_void_p, C.c_size_t,
+                                      C.c_char_p, C.POINTER(C.c_uint64)]
     L.sw_meet_check_order.argtypes = [C.c_uint32, _u64p, C.c_size_t, _u64p, C.c_size_t,
                                       C.c_uint32, _u32p]
     L.sw_heuristic.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_int32, C.c_uint64, C.c_uint64,
@@ -344,7 +366,7 @@ def default_options(**kw) -> SolveOptions:
     for key, v in kw.items():
         if key == "schedule" and isinstance(v, str):
             v = SCHEDULES[v]
-        if key in ("track_word", "timing", "contain_stats"):
+        if key in ("track_word", "timing", "contain_stats", "dfs_reference_order"):
             v = int(bool(v))
         if v is None:
             continue
@@ -388,6 +410,70 @@ def list_trie_exists(n: int, a_words, b_words):
     _check(load().sw_list_trie_exists(n, a, a.size // W, b, b.size // W, C.byref(m), C.byref(ai),
                                       C.byref(bi)))
     return bool(m.value), int(ai.value), int(bi.value)
+
+
+# ------------------------------------------------------- partitioned solve
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(load().sw_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """A communicator for sw_solve_exact_dist: NCCL on device buffers
+    (nccl_id from nccl_unique_id() on one rank, shared by the caller) or host
+    callbacks (callbacks=(all_to_allv, all_gather_v, all_reduce_u64) with the
+    C signatures of include/synchro_b200.h)."""
+
+    def __init__(self, rank: int, nranks: int, nccl_id: Optional[bytes] = None, callbacks=None):
+        d = CommDesc()
+        d.rank, d.nranks = rank, nranks
+        if nccl_id is not None:
+            d.kind = SW_COMM_NCCL
+            C.memmove(d.nccl_id, nccl_id, min(128, len(nccl_id)))
+        else:
+            d.kind = SW_COMM_CALLBACK
+            self._cbs = (A2A_CB(callbacks[0]), AG_CB(callbacks[1]), AR_CB(callbacks[2]))
+            d.all_to_allv, d.all_gather_v, d.all_reduce_u64 = self._cbs
+        self._h = C.c_void_p()
+        _check(load().sw_comm_create(C.byref(d), C.byref(self._h)))
+        self.rank, self.nranks = rank, nranks
+
+    def close(self):
+        if self._h:
+            load().sw_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_exact_dist(aut: Automaton, comm: Comm, trace_path: Optional[str] = None, **opts):
+    """Partitioned sw_solve_exact_dist: (SolveResult, NVLink/transport bytes sent by this rank)."""
+    o = default_options(**opts)
+    r = SolveResultC()
+    cap = 1 << 20 if o.track_word else 0
+    buf = np.zeros(max(cap, 1), np.uint32)
+    nv = C.c_uint64()
+    _check(load().sw_solve_exact_dist(aut.n, aut.k, np.ascontiguousarray(aut.delta, np.uint32),
+                                      C.byref(o), comm._h, C.byref(r),
+                                      buf.ctypes.data_as(C.c_void_p), cap,
+                                      trace_path.encode() if trace_path else None, C.byref(nv)))
+    word = buf[: r.word_len].tolist() if r.has_word else None
+    trace = None
+    if trace_path and os.path.exists(trace_path):
+        with open(trace_path) as f:
+            trace = f.read().splitlines()
+    res = SolveResult(r.threshold, word, r.upper_bound, r.iterations, r.bfs_steps, r.ibfs_steps,
+                      bool(r.used_dfs), r.peak_memory, r.expansions_phase1, r.expansions_dfs,
+                      r.heuristic_seconds, r.engine_seconds, r.expand_kernel_ms,
+                      r.kernel_launches, r.phase.decode(), r.engine_device_ms, r.h2d_bytes,
+                      r.d2h_bytes, r.contain_kernel_ms, r.contain_bytes, trace,
+                      r.contain_visits, r.contain_pairs)
+    return res, int(nv.value)
 
 
 def meet_check_order(n: int, a_words, b_words, min_brute: int = 64) -> np.ndarray:

@@ -152,3 +152,65 @@ def test_owner_hash_is_a_function_of_the_row():
     a = owner_hash(rows.reshape(-1), 2, 8)
     b = owner_hash(np.concatenate([rows, rows[::-1]]).reshape(-1), 2, 8)
     assert (a == b[:20]).all() and (a[::-1] == b[20:]).all() and set(a.tolist()) <= set(range(8))
+
+
+CALLBACK_WORKER = r"""
+import ctypes as C, json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import torch.distributed as dist
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]),
+                        world_size={world})
+rank, world = dist.get_rank(), dist.get_world_size()
+from paper_2207_05495_b200 import distributed, native
+cb = distributed.TorchCallbacks()
+# exactly the C signatures of sw_comm (include/synchro_b200.h), through ctypes thunks
+a2a = native.A2A_CB(cb.all_to_allv)
+ag = native.AG_CB(cb.all_gather_v)
+ar = native.AR_CB(cb.all_reduce_u64)
+# all_to_allv: rank r sends (r*10 + d) repeated (d+1) times to rank d
+send = np.concatenate([np.full(d + 1, rank * 10 + d, np.uint8) for d in range(world)])
+sb = (C.c_uint64 * world)(*[d + 1 for d in range(world)])
+rb = (C.c_uint64 * world)(*[rank + 1 for _ in range(world)])
+recv = np.zeros(sum(rb), np.uint8)
+assert a2a(None, send.ctypes.data, sb, recv.ctypes.data, rb) == 0
+# all_gather_v: rank r contributes r+1 bytes of value 100+r
+mine = np.full(rank + 1, 100 + rank, np.uint8)
+gb = (C.c_uint64 * world)(*[r + 1 for r in range(world)])
+gath = np.zeros(sum(gb), np.uint8)
+assert ag(None, mine.ctypes.data, mine.size, gath.ctypes.data, gb) == 0
+# all_reduce_u64 sum / min / max
+out = {{}}
+for op in (0, 1, 2):
+    v = (C.c_uint64 * 2)(rank + 5, 1000 - rank)
+    assert ar(None, v, 2, op) == 0
+    out[op] = list(v)
+print(json.dumps({{"recv": recv.tolist(), "gath": gath.tolist(), "red": out}}))
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_solve_host_collectives_gloo(world):
+    """The host-buffer collectives the partitioned solve calls through sw_comm
+    (distributed.TorchCallbacks over gloo, invoked via the C function-pointer
+    types): variable-size all-to-all, all-gather and u64 all-reduces."""
+    import json
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    code = CALLBACK_WORKER.format(root=ROOT, port=port, world=world)
+    procs = [subprocess.Popen([sys.executable, "-c", code, str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(world)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-2000:]
+    res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
+    for r, x in enumerate(res):
+        assert x["recv"] == [v for src in range(world) for v in [src * 10 + r] * (r + 1)]
+        assert x["gath"] == [v for src in range(world) for v in [100 + src] * (src + 1)]
+        assert x["red"]["0"] == [sum(q + 5 for q in range(world)), sum(1000 - q for q in range(world))]
+        assert x["red"]["1"] == [5, 1000 - (world - 1)]
+        assert x["red"]["2"] == [world + 4, 1000]

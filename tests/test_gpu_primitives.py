@@ -298,8 +298,9 @@ print("BAD", bad)
 """
 
 
+@pytest.mark.parametrize("index", ["", "trie"])
 @pytest.mark.parametrize("spill_cap", ["0", "128"])
-def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap):
+def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap, index):
     """contain.cu: when a warp's task pool and its spill stack are both full, the
     opened range is scanned instead of descended.  SYNCHRO_SPILL_CAP shrinks the
     stack so that path runs (the progress log counts overflow scans); marks,
@@ -309,6 +310,8 @@ def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, SYNCHRO_SPILL_CAP=spill_cap, SYNCHRO_PROGRESS="1")
+    if index:  # marking through the trie index too (device/trie_query.cu)
+        env["SYNCHRO_INDEX"] = index
     p = subprocess.run([sys.executable, "-c", _OVERFLOW_PROBE, root], env=env,
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
