@@ -314,6 +314,7 @@ struct TrieQueryIndex {
   void* keysig = nullptr;   // per-key filter words
   uint8_t* state_bit = nullptr;  // state -> filter bit (the 64 most frequent key states), 255: none
   u32 root_div = 0xFFFF;         // the root's division state (0xFFFF: the root is a leaf)
+  void* psig = nullptr;          // per node: AND of each payload's key filter words (2 x 16 B)
 };
 u64 build_trie_nodes(Context& c, const DList& l, u32 min_leaf, TrieQueryIndex* qi);  // internal
 TrieQueryIndex build_trie_index(Context& c, const DList& a, u32 leaf_keys);

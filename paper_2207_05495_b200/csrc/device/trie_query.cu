@@ -38,6 +38,10 @@ constexpr int kCap = 256;        // tasks per warp in shared memory
 constexpr int kSpillHalf = kCap / 2;
 constexpr int kSpillCap = 1024;  // tasks per warp in the global spill stack
 constexpr int kHitSlots = 32;
+#ifndef SW_PAYLOAD_SIG
+#define SW_PAYLOAD_SIG 0
+#endif
+constexpr bool kPayloadSig = SW_PAYLOAD_SIG != 0;
 
 template <int W>
 struct Pad {
@@ -113,6 +117,32 @@ __global__ void trie_pad_kernel(const u64* __restrict__ src, const u32* __restri
   }
 }
 
+// Per node, the AND of the filter words of each payload (zero side absorbed,
+// one side a leaf): every key of the payload holds those bits, so a query
+// lacking one of them skips the whole payload scan (one 32-byte load instead
+// of up to kTrieLeafKeys key filters).  Measured: no gain at n=300 or n=570
+// (the extra load per visit cancels the skipped scans) — off by default.
+__global__ void payload_sig_kernel(const TrieNode* __restrict__ nodes, u64 count,
+                                   const ulonglong2* __restrict__ ksig, ulonglong2* __restrict__ psig) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const TrieNode nd = nodes[i];
+    ulonglong2 z = make_ulonglong2(~0ull, ~0ull), o = make_ulonglong2(~0ull, ~0ull);
+    if (nd.zero == kNo)
+      for (u32 k = nd.lo; k < nd.mid; ++k) {
+        z.x &= ksig[k].x;
+        z.y &= ksig[k].y;
+      }
+    if (nd.one == kNo)
+      for (u32 k = nd.mid; k < nd.hi; ++k) {
+        o.x &= ksig[k].x;
+        o.y &= ksig[k].y;
+      }
+    psig[2 * i] = z;
+    psig[2 * i + 1] = o;
+  }
+}
+
 __global__ void map_flags_kernel(const uint8_t* __restrict__ src, const u32* __restrict__ perm,
                                  u64 count, uint8_t* __restrict__ dst) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
@@ -125,8 +155,9 @@ __global__ void map_flags_kernel(const uint8_t* __restrict__ src, const u32* __r
 template <int W, bool PROPER, bool EXIST>
 __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) trie_pool_kernel(
     const u64* __restrict__ K, const ulonglong2* __restrict__ Ksig,
-    const TrieNode* __restrict__ nodes, const u64* __restrict__ Q,
-    const ulonglong2* __restrict__ Qsig, u32 Nq, uint8_t* keep, int* found,
+    const TrieNode* __restrict__ nodes, const ulonglong2* __restrict__ psig,
+    const u64* __restrict__ Q, const ulonglong2* __restrict__ Qsig, u32 Nq, uint8_t* keep,
+    int* found,
     unsigned long long* wit, u32* next_query, uint4* spill_all, u32* overflow_scans,
     unsigned long long* stats, u32 root_div, u32 spill_cap) {
   constexpr int P = Pad<W>::P;
@@ -215,19 +246,24 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
     // ---- one round of independent loads: the node, the query's filter words
     // and the query word holding the node's division state (carried by the task)
     TrieNode nd{};
-    ulonglong2 qs = make_ulonglong2(0, 0);
+    ulonglong2 qs = make_ulonglong2(0, 0), zsig = make_ulonglong2(0, 0),
+               osig = make_ulonglong2(0, 0);
     u64 yw = 0;
     if (have) {
       nd = load_trie_node(nodes + id);
       qs = __ldg(Qsig + j);
       if (dv != 0xFFFF) yw = __ldg(Q + static_cast<u64>(j) * P + (dv >> 6));
+      if (kPayloadSig) {
+        zsig = __ldg(psig + 2 * static_cast<u64>(id));
+        osig = __ldg(psig + 2 * static_cast<u64>(id) + 1);
+      }
     }
     // ---- evaluate: zero side always, one side iff y holds the division state
     u32 c0 = kNo, c1 = kNo, zlo = 0, zn = 0, olo = 0, on = 0;
     if (have && nd.minc <= limit) {
       if (nd.zero != kNo) {
         c0 = nd.zero;
-      } else {
+      } else if (!kPayloadSig || sig_pass(zsig, qs)) {
         zlo = nd.lo;
         zn = nd.mid - nd.lo;
       }
@@ -235,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
         if ((yw >> (63 - (dv & 63))) & 1) {
           if (nd.one != kNo) {
             c1 = nd.one;
-          } else {
+          } else if (!kPayloadSig || sig_pass(osig, qs)) {
             olo = nd.mid;
             on = nd.hi - nd.mid;
           }
@@ -405,7 +441,7 @@ void launch(Context& c, const TrieQueryIndex& t, const u64* Qrows, const void* Q
   SW_DISPATCH_W(c.W(), {
     trie_pool_kernel<W, PROPER, EXIST><<<grid, kThreads, 0, s>>>(
         t.keys, static_cast<const ulonglong2*>(t.keysig), static_cast<const TrieNode*>(t.nodes),
-        Qrows, static_cast<const ulonglong2*>(Qsig), static_cast<u32>(Nq), keep, found, wit,
+        static_cast<const ulonglong2*>(t.psig), Qrows, static_cast<const ulonglong2*>(Qsig), static_cast<u32>(Nq), keep, found, wit,
         counter, spill, counter + 1, stats, t.root_div, spill_cap);
   });
   SW_CHECK_LAUNCH();
@@ -446,6 +482,7 @@ TrieQueryIndex::~TrieQueryIndex() {
       ctx->free(keys);
       ctx->free(keysig);
       ctx->free(state_bit);
+      ctx->free(psig);
     } catch (...) {
     }
   }
@@ -459,6 +496,7 @@ TrieQueryIndex& TrieQueryIndex::operator=(TrieQueryIndex&& o) noexcept {
       ctx->free(keys);
       ctx->free(keysig);
       ctx->free(state_bit);
+      ctx->free(psig);
     }
     ctx = o.ctx;
     count = o.count;
@@ -469,6 +507,8 @@ TrieQueryIndex& TrieQueryIndex::operator=(TrieQueryIndex&& o) noexcept {
     keysig = o.keysig;
     state_bit = o.state_bit;
     root_div = o.root_div;
+    psig = o.psig;
+    o.psig = nullptr;
     o.ctx = nullptr;
     o.nodes = nullptr;
     o.order = nullptr;
@@ -510,6 +550,11 @@ TrieQueryIndex build_trie_index(Context& c, const DList& a, u32 leaf_keys) {
     t.keys = pad_queries<W>(c, t, a, t.order, &sig);
     t.keysig = sig;
   });
+  t.psig = c.alloc(static_cast<size_t>(t.node_count) * 32);
+  payload_sig_kernel<<<grid_for(t.node_count, 256), 256, 0, as_stream(c.stream())>>>(
+      static_cast<const TrieNode*>(t.nodes), t.node_count, static_cast<const ulonglong2*>(t.keysig),
+      static_cast<ulonglong2*>(t.psig));
+  SW_CHECK_LAUNCH();
   SYNCHRO_PROGRESS("  trie-index |A|=%zu nodes=%llu", a.size(),
                    static_cast<unsigned long long>(t.node_count));
   return t;
