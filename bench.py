@@ -367,7 +367,8 @@ def run_ours(args, world, rank, local):
         # meet check, DFS queries).  Algorithmic bytes = every key and query row
         # read once; it is a latency-bound tree walk (ncu: L1/TEX-throughput bound,
         # profiles/), so its HBM fraction is small by nature.
-        "roofline": {"bound": "hbm", "kernel": "contain_pool_kernel (containment traversal)",
+        "roofline": {"bound": "hbm", "kernel": "containment traversal (contain_pool_kernel marking "
+                                                "+ trie_pool_kernel existence queries)",
                      "achieved": cont_gbs, "peak": roof_peak, "unit": "GB/s",
                      "frac": (cont_gbs / roof_peak) if cont_gbs else None,
                      "traffic": traffic["contain"], "traffic_note": traffic["contain_note"],
@@ -425,12 +426,16 @@ def dram_traffic(W, cont_bytes_per_solve):
     """roofline.traffic: DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per
     launch from the committed ncu captures of the same kernels on the same workload
     (profiles/r01_dram_traffic.json, made by scripts/traffic_summary.py), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_dram_traffic.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
     out = {"contain": None, "contain_note": None, "expand": None, "dedupe": None}
     if not os.path.exists(path):
         return out
     t = json.load(open(path))
-    cont = [v for k, v in t.items() if k.startswith(f"contain_pool_kernel<{W},")]
+    # the containment traversal: radix-tree marking + trie existence queries
+    cont = [v for k, v in t.items()
+            if k.startswith(f"contain_pool_kernel<{W},") or f"trie_pool_kernel<{W}," in k]
     if cont:
         launches = sum(v["launches"] for v in cont)
         tb = sum(v["traffic_bytes_per_launch"] * v["launches"] for v in cont)

@@ -575,6 +575,14 @@ class DfsRunner {
   }
   const DfsFind& find() const { return find_; }
   u64 expansions = 0;
+  // Progress mode: device+host seconds per DFS phase (expand, dedupe, window,
+  // query, sort, order replay), one stream sync per phase.
+  void report_phases() const {
+    if (!progress_enabled()) return;
+    SYNCHRO_PROGRESS("  dfs phases [s]: expand %.2f dedupe %.2f window %.2f query %.2f sort %.2f "
+                     "order-replay %.2f", phase_s_[0], phase_s_[1], phase_s_[2], phase_s_[3],
+                     phase_s_[4], phase_s_[5]);
+  }
 
  private:
   struct Frame {
@@ -596,7 +604,9 @@ class DfsRunner {
     ledger_.charge_or_throw(charged);
     Guard guard{ledger_, charged};
     DList next(&c_, (hi - lo) * k, tracking_);
+    phase_begin();
     dev::expand(c_, list, lo, hi, /*inverse=*/true, next);
+    phase_end(0);
     expansions += static_cast<u64>(hi - lo) * k;
     const u64 generated = next.size();
     // The reference sorts every level by (card desc, lex, index) (dfs_phase.hpp:105).
@@ -604,8 +614,11 @@ class DfsRunner {
     // as a multiset without sorting) and the slice boundaries (sorted only when the
     // level is sliced); the dedupe is set-semantic (which equal row's tag survives
     // changes only the reported witness), and the trie query is order-free.
+    phase_begin();
     if (t_.dfs_dedupe_cadence && level % t_.dfs_dedupe_cadence == 0)
       dev::hash_dedupe(c_, next, /*first_occurrence=*/false);  // any equal row's tag is a valid parent
+    phase_end(1);
+    phase_begin();
     if (t_.dfs_reduce_cadence && level % t_.dfs_reduce_cadence == 0 && next.size() > t_.dfs_largest) {
       // Drop sets that are proper subsets of one of the dfs_largest first
       // (largest) sets.  The reference marks proper supersets among
@@ -615,6 +628,7 @@ class DfsRunner {
       const DList largest = dev::top_card_desc_lex(c_, next, t_.dfs_largest);
       dev::remove_subsets_of(c_, largest, next, /*proper=*/true);
     }
+    phase_end(2);
     const u64 now = list_footprint(n, next.size());
     if (now < charged) {
       ledger_.release(charged - now);
@@ -626,16 +640,26 @@ class DfsRunner {
                      static_cast<unsigned long long>(r), level, hi - lo,
                      static_cast<unsigned long long>(generated), next.size());
     dev::Witness w;
-    if (query_(next, tracking_ ? &w : nullptr)) {
+    phase_begin();
+    const bool hit = query_(next, tracking_ ? &w : nullptr);
+    phase_end(3);
+    if (hit) {
       bound_ = r;
       if (tracking_) record_find(w, next, parent);
       return;
     }
     if (r >= bound_ - 1) return;
     const size_t cap = slice_cap(r);
-    if (next.size() > cap) {  // slices follow the order the trie queries left
+    // Slices follow the order the trie queries left (the reference's order).
+    // Relaxed order: any partition into slices keeps the threshold (every
+    // in-slice reduction keeps a dominating set), so the level is not sorted.
+    if (next.size() > cap && reference_order_) {
+      phase_begin();
       dev::sort_card_desc_lex(c_, next);
-      if (reference_order_) replay_query_order(next, cap);
+      phase_end(4);
+      phase_begin();
+      replay_query_order(next, cap);
+      phase_end(5);
     }
     const Frame frame{parent, &next};
     for (size_t plo = 0; plo < next.size(); plo += cap) {
@@ -720,6 +744,18 @@ class DfsRunner {
   DfsFind find_;
   std::set<u64> dumped_;
   std::unique_ptr<dev::TrieShape> shape_;  // the reference trie over L_BFS, built on first use
+  void phase_begin() {
+    if (!progress_enabled()) return;
+    c_.sync();
+    phase_t0_ = std::chrono::steady_clock::now();
+  }
+  void phase_end(int i) {
+    if (!progress_enabled()) return;
+    c_.sync();
+    phase_s_[i] += std::chrono::duration<double>(std::chrono::steady_clock::now() - phase_t0_).count();
+  }
+  std::chrono::steady_clock::time_point phase_t0_;
+  double phase_s_[6] = {0, 0, 0, 0, 0, 0};
 };
 
 }  // namespace
@@ -757,6 +793,7 @@ u64 GpuBibfs::run_dfs(u64 r, DfsFind* find, std::vector<std::array<u64, 5>>* log
   const u32 shards = dist() ? static_cast<u32>(opt_.comm->size())
                             : std::max<u32>(1, opt_.dfs_shard_count);
   u64 final_bound = dfs.run(*libfs_, r, R_, shard, shards);
+  dfs.report_phases();
   DfsFind mine = dfs.find();
   u64 exp = dfs.expansions;
   if (dist()) {

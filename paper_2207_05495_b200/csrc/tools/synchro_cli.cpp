@@ -156,12 +156,15 @@ int cmd_exact(int argc, char** argv) {
                             join(join(kSource, kTuning), {"--memory", "--time-limit", "--threads",
                                                           "--schedule", "--trace", "--device",
                                                           "--dfs-shard"}),
-                            {"--track-word"});
+                            {"--track-word", "--relaxed-dfs-order"});
   SolveOptions opt;
   if (a.has("--memory")) opt.memory = to_u64(a.get("--memory"), "--memory");
   const double tl = a.has("--time-limit") ? to_double(a.get("--time-limit"), "--time-limit") : 0.0;
   if (tl > 0) opt.time_limit = tl;
   opt.track_word = a.has("--track-word");
+  // DFS slices of the unsorted level instead of the reference's exact order:
+  // same threshold, different DFS level sizes, no host-side order replay.
+  opt.dfs_reference_order = !a.has("--relaxed-dfs-order");
   const std::string sched = a.get("--schedule", "auto");
   if (sched == "bfs") opt.schedule = Schedule::BfsOnly;
   else if (sched == "ibfs") opt.schedule = Schedule::IbfsOnly;
