@@ -10,7 +10,8 @@
 // space the question is a superset query, and every x ⊇ y contains y's
 // rarest state r(y).  So:
 //   1. hist = per-state counts over X (bit-sliced);
-//   2. r(y) = the state of y with the fewest X-sets (ties: smallest index);
+//   2. r(y) = the state of y with the fewest X-sets (ties: smallest index),
+//      found by probing the states in ascending-count order;
 //   3. candidate buckets C_r = {x ∋ r}, sorted by |x| descending (one radix
 //      sort of (r, ~|x|) keys over the needed buckets);
 //   4. queries sorted by (r(y), |y|); one CTA per 128 queries of a bucket
@@ -36,30 +37,42 @@ namespace {
 constexpr int kJoinThreads = 128;  // queries per CTA
 constexpr int kJoinTile = 128;     // candidate rows staged per pass
 
-// r(y) and the sort key (r << 11 | |y|) of every query; r = n for y = ∅.
+// r(y) and the sort key (r << 11 | |y|) of every query (r = n for y = ∅), by
+// probing the states in ascending X-frequency order (ties: smaller state
+// first) until y holds one — the first hit is y's rarest state.  For
+// the dense queries of the DFS window (a third of the states) that is a few
+// probes instead of a walk over every set bit.
 template <int W>
-__global__ void rarest_kernel(const u64* __restrict__ Y, const u32* __restrict__ Ycard, u64 ny,
-                              u32 n, const u32* __restrict__ hist, u32* __restrict__ key,
-                              u32* __restrict__ idx) {
+__global__ void rarest_probe_kernel(const u64* __restrict__ Y, const u32* __restrict__ Ycard,
+                                    u64 ny, u32 n, const uint16_t* __restrict__ g_order,
+                                    u32* __restrict__ key, u32* __restrict__ idx) {
+  extern __shared__ uint16_t s_order[];
+  for (u32 i = threadIdx.x; i < n; i += blockDim.x) s_order[i] = g_order[i];
+  __syncthreads();
   for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < ny;
        j += static_cast<u64>(gridDim.x) * blockDim.x) {
-    u32 best = n, best_f = 0xFFFFFFFFu;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      u64 bits = Y[j * W + w];
-      while (bits) {
-        const int b = __clzll(bits);
-        bits &= ~(u64{1} << (63 - b));
-        const u32 q = w * 64 + b;
-        const u32 f = hist[q];
-        if (f < best_f) {  // ascending q: strict < keeps the smallest state
-          best_f = f;
+    u32 best = n;
+    if (Ycard[j])
+      for (u32 i = 0; i < n; ++i) {
+        const u32 q = s_order[i];
+        if ((__ldg(Y + j * W + (q >> 6)) >> (63 - (q & 63))) & 1) {
           best = q;
+          break;
         }
       }
-    }
     key[j] = (best << 11) | min(Ycard[j], 2047u);
     idx[j] = static_cast<u32>(j);
+  }
+}
+
+// Query range of every bucket in the (r, |y|)-sorted keys (lo[r], hi[r]).
+__global__ void bucket_bounds_kernel(const u32* __restrict__ key, u64 ny, u32* __restrict__ lo,
+                                     u32* __restrict__ hi) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < ny;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 r = key[i] >> 11;
+    if (i == 0 || (key[i - 1] >> 11) != r) lo[r] = static_cast<u32>(i);
+    if (i + 1 == ny || (key[i + 1] >> 11) != r) hi[r] = static_cast<u32>(i + 1);
   }
 }
 
@@ -191,16 +204,25 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
     timer = std::make_unique<StreamTimer>(c);
     timer->start();
   }
-  // 1. per-state counts over X
+  // 1. per-state counts over X, and the states in ascending-count order
   u32* hist = static_cast<u32*>(c.alloc(n * 4));
   state_histogram(c, X, hist);
+  std::vector<u32> hhist(n);
+  c.memcpy_d2h(hhist.data(), hist, n * 4);
+  std::vector<uint16_t> order(n);
+  std::iota(order.begin(), order.end(), static_cast<uint16_t>(0));
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint16_t a, uint16_t b) { return hhist[a] < hhist[b]; });
+  uint16_t* dorder = static_cast<uint16_t*>(c.alloc(n * 2));
+  c.memcpy_h2d(dorder, order.data(), n * 2);
   // 2. rarest state of every query; sort queries by (r, |y|)
   u32* qkey = static_cast<u32*>(c.alloc(ny * 4));
   u32* qkey2 = static_cast<u32*>(c.alloc(ny * 4));
   u32* qidx = static_cast<u32*>(c.alloc(ny * 4));
   u32* qidx2 = static_cast<u32*>(c.alloc(ny * 4));
   SW_DISPATCH_W(c.W(), {
-    rarest_kernel<W><<<grid_for(ny, 256), 256, 0, s>>>(Y.words, Y.cards, ny, n, hist, qkey, qidx);
+    rarest_probe_kernel<W><<<grid_for(ny, 256), 256, n * 2, s>>>(Y.words, Y.cards, ny, n, dorder,
+                                                                  qkey, qidx);
   });
   SW_CHECK_LAUNCH();
   int keybits = 11;
@@ -217,19 +239,20 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
     qkey2 = k.Alternate();
     qidx2 = v.Alternate();
   }
-  // per-bucket query ranges (host: n buckets)
-  std::vector<u32> hkey(ny);
-  c.memcpy_d2h(hkey.data(), qkey, ny * 4);
-  std::vector<u32> hhist(n);
-  c.memcpy_d2h(hhist.data(), hist, n * 4);
+  // per-bucket query ranges (device; n + 1 buckets come back)
   std::vector<u32> qlo(n + 1, 0), qhi(n + 1, 0);
-  for (u64 i = 0; i < ny;) {
-    const u32 r = hkey[i] >> 11;
-    u64 e = i;
-    while (e < ny && (hkey[e] >> 11) == r) ++e;
-    qlo[r] = static_cast<u32>(i);
-    qhi[r] = static_cast<u32>(e);
-    i = e;
+  {
+    u32* dlh = static_cast<u32*>(c.alloc(2ull * (n + 1) * 4));
+    SW_CUDA(cudaMemsetAsync(dlh, 0, 2ull * (n + 1) * 4, s));
+    bucket_bounds_kernel<<<grid_for(ny, 256), 256, 0, s>>>(qkey, ny, dlh, dlh + n + 1);
+    SW_CHECK_LAUNCH();
+    std::vector<u32> h(2ull * (n + 1));
+    c.memcpy_d2h(h.data(), dlh, h.size() * 4);
+    c.free(dlh);
+    for (u32 r = 0; r <= n; ++r) {
+      qlo[r] = h[r];
+      qhi[r] = h[n + 1 + r];
+    }
   }
   std::vector<uint8_t> need(n, 0);
   for (u32 r = 0; r < n; ++r) need[r] = (qhi[r] > qlo[r] && hhist[r] > 0) ? 1 : 0;
@@ -311,6 +334,7 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
   }
   c.counters.kernel_launches += 8;
   c.free(hist);
+  c.free(dorder);
   c.free(qkey);
   c.free(qkey2);
   c.free(qidx);
