@@ -522,6 +522,13 @@ SW_EXPORT int sw_list_mark(uint32_t n, const uint64_t* a_words, size_t a_count,
     dev::Context c(identity_aut(n));
     dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    if (dev::bitmap_fits(c) && mode != 2) {  // n <= 20: the power-set bitmap
+      uint8_t* dkeep = static_cast<uint8_t*>(c.alloc(std::max<size_t>(b_count, 1)));
+      if (b_count) dev::bitmap_keep_flags(c, a, b, /*super=*/false, mode == 1, dkeep);
+      c.memcpy_d2h(keep, dkeep, b_count);
+      c.free(dkeep);
+      return;
+    }
     if (mode == 2) {  // subsets of some a element: the bucketed superset join
       uint8_t* dkeep = static_cast<uint8_t*>(c.alloc(std::max<size_t>(b_count, 1)));
       dev::superset_keep_flags(c, a, b, /*proper=*/false, dkeep);
@@ -553,6 +560,10 @@ SW_EXPORT int sw_list_meet_check(uint32_t n, const uint64_t* a_words, size_t a_c
     dev::Context c(identity_aut(n));
     dev::DList a = dev::upload(c, a_words, nullptr, nullptr, a_count);
     dev::DList b = dev::upload(c, b_words, nullptr, nullptr, b_count);
+    if (dev::bitmap_fits(c)) {
+      *met = dev::bitmap_exists_subset(c, a, b, nullptr) ? 1 : 0;
+      return;
+    }
     if (dev::use_trie_index()) {
       const dev::TrieQueryIndex t = dev::build_trie_index(c, a, dev::kTrieLeafKeys);
       *met = dev::trie_exists_subset(c, t, b, nullptr) ? 1 : 0;

@@ -921,6 +921,12 @@ std::vector<uint8_t> superset_keep(Context& c, const PermIndex& p, const DList& 
 // Rarest-state-first order prunes best here (queries are the keys themselves).
 size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper) {
   if (b.empty() || A.empty()) return 0;
+  if (bitmap_fits(c)) {  // n <= 20: the power-set bitmap
+    const size_t before = b.size();
+    auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
+    bitmap_keep_flags(c, A, b, /*super=*/false, proper, keep);
+    return before - compact_flags(c, b, keep, nullptr);
+  }
   if (brute_fits(A.size(), b.size())) {
     const size_t before = b.size();
     auto* keep = static_cast<uint8_t*>(c.scratch(5, b.size()));
@@ -940,6 +946,12 @@ size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper) {
 
 size_t self_reduce_minimal(Context& c, DList& l) {
   if (l.size() <= 1) return 0;
+  if (bitmap_fits(c)) {  // n <= 20: the power-set bitmap
+    const size_t before = l.size();
+    auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));
+    bitmap_keep_flags(c, l, l, /*super=*/false, /*proper=*/true, keep);
+    return before - compact_flags(c, l, keep, nullptr);
+  }
   if (brute_fits(l.size(), l.size())) {  // small list: one all-pairs launch
     const size_t before = l.size();
     auto* keep = static_cast<uint8_t*>(c.scratch(5, l.size()));

@@ -239,6 +239,17 @@ bool brute_exists_subset(Context& c, const DList& A, const DList& B, Witness* w)
 // FreqDesc index over A.  Returns #removed.
 size_t remove_supersets_of(Context& c, const DList& A, DList& b, bool proper);
 
+// ---- containment over the whole power set (bitmap.cu), n <= kBitmapMaxStates:
+// one single-CTA launch per question (shared-memory bitmap of all 2^n sets,
+// subset-/superset-OR transform, n lookups per query).
+constexpr u32 kBitmapMaxStates = 20;
+bool bitmap_fits(const Context& c);
+// keep[j] = 1 iff no a in A relates to B[j] (as brute_keep_flags).
+void bitmap_keep_flags(Context& c, const DList& A, const DList& B, bool super, bool proper,
+                       uint8_t* keep);
+// Is some a ⊆ some b?  *b_index = a b with a subset in A.
+bool bitmap_exists_subset(Context& c, const DList& A, const DList& B, size_t* b_index);
+
 // ---- list surgery
 void keep_card_at_most(Context& c, DList& l, u32 max_card);
 void keep_card_at_least(Context& c, DList& l, u32 min_card);  // plain card of complements
@@ -328,7 +339,10 @@ size_t trie_self_reduce_minimal(Context& c, DList& l);
 // (default) or the relabelled radix tree (SYNCHRO_INDEX=radix, A/B only).
 bool use_trie_index();       // existence queries
 bool use_trie_for_marks();   // marking (self-reduction, history)
-constexpr u32 kTrieLeafKeys = 16;
+#ifndef SW_TRIE_LEAF
+#define SW_TRIE_LEAF 16
+#endif
+constexpr u32 kTrieLeafKeys = SW_TRIE_LEAF;  // payload size of the query trie (a performance knob)
 
 // ---- microbenchmarks (microbench.cu): avg CUDA-event ms per call on `count`
 // device-generated random sets of the given density.

@@ -192,6 +192,14 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
   const u64 ny = Y.size(), nx = X.size();
   cudaStream_t s = as_stream(c.stream());
   if (!ny) return;
+  if (bitmap_fits(c)) {  // n <= 20: the power-set bitmap
+    if (!nx) {
+      SW_CUDA(cudaMemsetAsync(keep, 1, ny, s));
+      return;
+    }
+    bitmap_keep_flags(c, X, Y, /*super=*/true, proper, keep);
+    return;
+  }
   if (brute_fits(nx, ny)) {  // small lists: one all-pairs launch
     brute_keep_flags(c, X, Y, /*super=*/true, proper, keep);
     return;

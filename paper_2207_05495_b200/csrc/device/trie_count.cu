@@ -178,7 +178,7 @@ __global__ void emit_kernel(const Seg* __restrict__ segs, u32 nact, const u32* _
   const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nact) return;
   const Seg sg = segs[i];
-  const u32 zeros = zc[i], ones = sg.hi - sg.lo - zeros;
+  const u32 zeros = zc[i];
   TrieNode nd;
   nd.div = div[i];
   nd.minc = minc[i];

@@ -256,6 +256,18 @@ const dev::TrieQueryIndex& GpuBibfs::bfs_trie() {
 
 // Is some L_BFS set a subset of some set of b?  (meet_check / trie query)
 bool GpuBibfs::exists_in_bfs(const DList& b, dev::Witness* w) {
+  if (dev::bitmap_fits(ctx_)) {  // n <= 20: the power-set bitmap, then the witness's subset
+    size_t bi = 0;
+    if (!dev::bitmap_exists_subset(ctx_, *lbfs_, b, &bi)) return false;
+    if (w) {
+      const DList one = dev::slice_copy(ctx_, b, bi, bi + 1, false);
+      dev::Witness w1;
+      dev::brute_exists_subset(ctx_, *lbfs_, one, &w1);
+      w->a_index = w1.a_index;
+      w->b_index = bi;
+    }
+    return true;
+  }
   if (dev::use_trie_index()) return dev::trie_exists_subset(ctx_, bfs_trie(), b, w);
   return dev::exists_subset(ctx_, bfs_index(), b, w);
 }
@@ -443,14 +455,14 @@ bool GpuBibfs::meet() {
     const DList ibfs = gather(*libfs_, false);
     bool met = false;
     if (!lbfs_->empty() && !ibfs.empty())
-      met = dev::brute_fits(lbfs_->size(), ibfs.size())
+      met = dev::brute_fits(lbfs_->size(), ibfs.size()) && !dev::bitmap_fits(ctx_)
                 ? dev::brute_exists_subset(ctx_, *lbfs_, ibfs, nullptr)
                 : exists_in_bfs(ibfs, nullptr);
     return allsum(met ? 1 : 0) > 0;
   }
   lbfs_met_ = !opt_.track_word;  // meet_check permutes L_IBFS (subset_algebra.hpp:201-210)
   if (hopeless) return false;
-  if (dev::brute_fits(lbfs_->size(), libfs_->size()))
+  if (dev::brute_fits(lbfs_->size(), libfs_->size()) && !dev::bitmap_fits(ctx_))
     return dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, nullptr);
   return exists_in_bfs(*libfs_, nullptr);
 }
@@ -462,7 +474,7 @@ bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
     dev::Witness w;
     bool met = false;
     if (!lbfs_->empty() && !ibfs.empty())
-      met = dev::brute_fits(lbfs_->size(), ibfs.size())
+      met = dev::brute_fits(lbfs_->size(), ibfs.size()) && !dev::bitmap_fits(ctx_)
                 ? dev::brute_exists_subset(ctx_, *lbfs_, ibfs, &w)
                 : exists_in_bfs(ibfs, &w);
     const u64 off = rank_offset(*lbfs_);
@@ -480,7 +492,7 @@ bool GpuBibfs::meet_witness(size_t* bfs_index_out, u64* ibfs_tag) {
     return true;
   }
   dev::Witness w;
-  const bool met = dev::brute_fits(lbfs_->size(), libfs_->size())
+  const bool met = dev::brute_fits(lbfs_->size(), libfs_->size()) && !dev::bitmap_fits(ctx_)
                        ? dev::brute_exists_subset(ctx_, *lbfs_, *libfs_, &w)
                        : exists_in_bfs(*libfs_, &w);
   if (!met) return false;

@@ -150,7 +150,9 @@ def test_self_reduce_minimal(gpu, ref, n, density, count):
 
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("n,da,db", [(30, 0.2, 0.5), (100, 0.05, 0.3), (300, 0.05, 0.2),
-                                     (300, 0.9, 0.95), (570, 0.03, 0.2)])
+                                     (300, 0.9, 0.95), (570, 0.03, 0.2),
+                                     # n <= 20: the power-set bitmap path (bitmap.cu)
+                                     (20, 0.3, 0.6), (13, 0.4, 0.5), (4, 0.5, 0.5), (1, 0.5, 0.5)])
 def test_mark_modes(gpu, ref, mode, n, da, db):
     a = lex_sorted_unique(n, random_list(n, 4000, da, 1))
     b = random_list(n, 6000, db, 2)
@@ -169,7 +171,8 @@ def test_mark_rejects_unsorted_a(gpu):
 
 
 @pytest.mark.parametrize("n,da,db,seed", [(100, 0.1, 0.4, 0), (300, 0.08, 0.3, 1),
-                                          (300, 0.08, 0.1, 2), (64, 0.3, 0.3, 3)])
+                                          (300, 0.08, 0.1, 2), (64, 0.3, 0.3, 3),
+                                          (20, 0.3, 0.4, 4), (9, 0.4, 0.3, 5)])
 def test_meet_check(gpu, ref, n, da, db, seed):
     a = lex_sorted_unique(n, random_list(n, 20000, da, seed))
     b = random_list(n, 2000, db, seed + 100)
