@@ -34,11 +34,19 @@ Context::Context(const Automaton& aut, int device) {
   cudaStream_t s;
   SW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   stream_ = s;
-  // Keep freed blocks in the pool: lists are re-allocated every level.
+  // A memory pool of its own (not the device's default one): the batch runner
+  // drives one context per worker thread, and allocations from a shared pool
+  // serialise on its lock.  Freed blocks stay in the pool (lists are
+  // re-allocated every level).
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device_;
   cudaMemPool_t pool;
-  SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
+  SW_CUDA(cudaMemPoolCreate(&pool, &props));
   u64 thresh = ~u64{0};
   SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  pool_ = pool;
   bind(aut);
 }
 
@@ -90,12 +98,13 @@ Context::~Context() {
   if (d_psrc) cudaFreeAsync(const_cast<void*>(d_psrc), as_stream(stream_));
   cudaStreamSynchronize(as_stream(stream_));
   cudaStreamDestroy(as_stream(stream_));
+  if (pool_) cudaMemPoolDestroy(static_cast<cudaMemPool_t>(pool_));
 }
 
 void* Context::alloc(size_t bytes) {
   if (bytes == 0) bytes = 16;
   void* p = nullptr;
-  SW_CUDA(cudaMallocAsync(&p, bytes, as_stream(stream_)));
+  SW_CUDA(cudaMallocFromPoolAsync(&p, bytes, static_cast<cudaMemPool_t>(pool_), as_stream(stream_)));
   return p;
 }
 

@@ -146,6 +146,7 @@ class Context {
   u32 n_ = 0, k_ = 0, W_ = 0;
   int device_ = 0;
   void* stream_ = nullptr;
+  void* pool_ = nullptr;  // cudaMemPool_t of this context
   struct Scratch { void* p = nullptr; size_t bytes = 0; };
   Scratch scratch_[11];  // slots: kernels.cuh
 };
@@ -257,7 +258,8 @@ void truncate(DList& l, size_t count);
 DList slice_copy(Context& c, const DList& l, size_t lo, size_t hi, bool tagged);
 // Rows start, start+stride, start+2·stride, ... (2D copies; no kernel).
 DList strided_copy(Context& c, const DList& l, size_t start, size_t stride, bool tagged);
-// h := sorted merge of disjoint lex-sorted unique lists h and add (untagged).
+// h := h ++ add (untagged): the merge of bibfs_engine.hpp:383-403 as a set
+// (every consumer of the histories is order-free; sort.cu).
 void merge_sorted(Context& c, DList& h, const DList& add);
 // l := rows perm[0], perm[1], ... of l (perm: device array of l.size() indices).
 void gather_rows(Context& c, DList& l, const u32* perm);

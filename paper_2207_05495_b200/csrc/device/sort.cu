@@ -171,6 +171,10 @@ size_t lex_sort_dedupe(Context& c, DList& l) {
   return before - compact_unique(c, l, perm);
 }
 
+// h := h ++ add.  The histories are only ever read by order-free consumers
+// (containment indexes build their own order; card filters and the ledger
+// see sets and sizes), so the reference's sorted merge (bibfs_engine.hpp:
+// 383-403) is a concatenation here: its size and set are the same.
 void merge_sorted(Context& c, DList& h, const DList& add) {
   if (add.empty()) return;
   const size_t total = h.size() + add.size();
@@ -184,8 +188,6 @@ void merge_sorted(Context& c, DList& h, const DList& add) {
   SW_CUDA(cudaMemcpyAsync(m.words + h.size() * W, add.words, add.size() * W * 8, cudaMemcpyDeviceToDevice, s));
   SW_CUDA(cudaMemcpyAsync(m.cards + h.size(), add.cards, add.size() * 4, cudaMemcpyDeviceToDevice, s));
   m.set_size(total);
-  // Disjoint sorted inputs: a stable lex sort of the concatenation is their merge.
-  sort_lex(c, m);
   h = std::move(m);
 }
 

@@ -18,6 +18,8 @@ namespace detail {
 
 using dev::DList;
 
+constexpr size_t kTrieMinKeys = 1 << 15;  // trie index for existence queries from this |L_BFS| on
+
 // ------------------------------------------------------------------ setup
 // L_BFS = [Q], H_BFS = [Q], L_IBFS = singletons tagged q, H_IBFS stored as
 // complements of the singletons; all four charged (bibfs_engine.hpp:68-95).
@@ -268,7 +270,10 @@ bool GpuBibfs::exists_in_bfs(const DList& b, dev::Witness* w) {
     }
     return true;
   }
-  if (dev::use_trie_index()) return dev::trie_exists_subset(ctx_, bfs_trie(), b, w);
+  // The trie's level-synchronous build (one round of launches per trie level)
+  // only pays off on large lists; small ones take the radix tree.
+  if (dev::use_trie_index() && lbfs_->size() >= kTrieMinKeys)
+    return dev::trie_exists_subset(ctx_, bfs_trie(), b, w);
   return dev::exists_subset(ctx_, bfs_index(), b, w);
 }
 
@@ -590,10 +595,18 @@ class DfsRunner {
   // Progress mode: device+host seconds per DFS phase (expand, dedupe, window,
   // query, sort, order replay), one stream sync per phase.
   void report_phases() const {
-    if (!progress_enabled()) return;
-    SYNCHRO_PROGRESS("  dfs phases [s]: expand %.2f dedupe %.2f window %.2f query %.2f sort %.2f "
-                     "order-replay %.2f", phase_s_[0], phase_s_[1], phase_s_[2], phase_s_[3],
-                     phase_s_[4], phase_s_[5]);
+    if (!phases_on()) return;
+    std::fprintf(stderr, "[synchro] dfs phases [s]: expand %.2f dedupe %.2f window %.2f query %.2f "
+                 "sort %.2f order-replay %.2f\n", phase_s_[0], phase_s_[1], phase_s_[2],
+                 phase_s_[3], phase_s_[4], phase_s_[5]);
+  }
+  // SYNCHRO_DFS_PHASES=1 (or the progress log): one stream sync per phase.
+  static bool phases_on() {
+    static const bool on = progress_enabled() || [] {
+      const char* e = std::getenv("SYNCHRO_DFS_PHASES");
+      return e && *e && *e != '0';
+    }();
+    return on;
   }
 
  private:
@@ -761,12 +774,12 @@ class DfsRunner {
   std::set<u64> dumped_;
   std::unique_ptr<dev::TrieShape> shape_;  // the reference trie over L_BFS, built on first use
   void phase_begin() {
-    if (!progress_enabled()) return;
+    if (!phases_on()) return;
     c_.sync();
     phase_t0_ = std::chrono::steady_clock::now();
   }
   void phase_end(int i) {
-    if (!progress_enabled()) return;
+    if (!phases_on()) return;
     c_.sync();
     phase_s_[i] += std::chrono::duration<double>(std::chrono::steady_clock::now() - phase_t0_).count();
   }
