@@ -34,16 +34,12 @@ Context::Context(const Automaton& aut, int device) {
   cudaStream_t s;
   SW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   stream_ = s;
-  // A memory pool of its own (not the device's default one): the batch runner
-  // drives one context per worker thread, and allocations from a shared pool
-  // serialise on its lock.  Freed blocks stay in the pool (lists are
-  // re-allocated every level).
-  cudaMemPoolProps props{};
-  props.allocType = cudaMemAllocationTypePinned;
-  props.location.type = cudaMemLocationTypeDevice;
-  props.location.id = device_;
+  // The device's default pool, keeping freed blocks (lists are re-allocated
+  // every level, and every solve_exact call creates a context: a pool of its
+  // own would start empty each time — measured: +100 ms per n=300 solve; it
+  // did not help the threaded batch runner either).
   cudaMemPool_t pool;
-  SW_CUDA(cudaMemPoolCreate(&pool, &props));
+  SW_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
   u64 thresh = ~u64{0};
   SW_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
   pool_ = pool;
@@ -98,7 +94,6 @@ Context::~Context() {
   if (d_psrc) cudaFreeAsync(const_cast<void*>(d_psrc), as_stream(stream_));
   cudaStreamSynchronize(as_stream(stream_));
   cudaStreamDestroy(as_stream(stream_));
-  if (pool_) cudaMemPoolDestroy(static_cast<cudaMemPool_t>(pool_));
 }
 
 void* Context::alloc(size_t bytes) {

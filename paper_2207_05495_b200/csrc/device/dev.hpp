@@ -146,7 +146,7 @@ class Context {
   u32 n_ = 0, k_ = 0, W_ = 0;
   int device_ = 0;
   void* stream_ = nullptr;
-  void* pool_ = nullptr;  // cudaMemPool_t of this context
+  void* pool_ = nullptr;  // cudaMemPool_t (the device's default pool)
   struct Scratch { void* p = nullptr; size_t bytes = 0; };
   Scratch scratch_[11];  // slots: kernels.cuh
 };
