@@ -57,8 +57,7 @@ void Context::bind(const Automaton& aut) {
     throw std::invalid_argument("n*k > 24576 transitions is not supported by the device kernels");
   SW_CUDA(cudaSetDevice(device_));
   if (d_img) free(const_cast<void*>(d_img));
-  if (d_poff) free(const_cast<void*>(d_poff));
-  if (d_psrc) free(const_cast<void*>(d_psrc));
+  d_img = nullptr;
   n_ = n;
   k_ = k;
   W_ = words_for(n);
@@ -66,22 +65,14 @@ void Context::bind(const Automaton& aut) {
   timing = false;
   contain_stats = false;
 
-  // Tables: image u16[k*n] at [a*n+q]; inverse CSR offsets u32[k*n+1], sources u16[n*k].
-  const InverseTransitions inv(aut);
+  // Image table u16[k*n] at [a*n+q].
   std::vector<uint16_t> img(static_cast<size_t>(k_) * n_);
   for (u32 a = 0; a < k_; ++a)
     for (u32 q = 0; q < n_; ++q) img[static_cast<size_t>(a) * n_ + q] = static_cast<uint16_t>(aut.next(q, a));
-  std::vector<uint32_t> off(inv.offsets().begin(), inv.offsets().end());
-  std::vector<uint16_t> src(inv.sources_flat().begin(), inv.sources_flat().end());
   void* p1 = alloc(img.size() * 2);
-  void* p2 = alloc(off.size() * 4);
-  void* p3 = alloc(src.size() * 2 + 2);
   memcpy_h2d(p1, img.data(), img.size() * 2);
-  memcpy_h2d(p2, off.data(), off.size() * 4);
-  memcpy_h2d(p3, src.data(), src.size() * 2);
   d_img = p1;
-  d_poff = p2;
-  d_psrc = p3;
+
   sync();
 }
 
@@ -90,8 +81,6 @@ Context::~Context() {
   for (auto& s : scratch_)
     if (s.p) cudaFreeAsync(s.p, as_stream(stream_));
   if (d_img) cudaFreeAsync(const_cast<void*>(d_img), as_stream(stream_));
-  if (d_poff) cudaFreeAsync(const_cast<void*>(d_poff), as_stream(stream_));
-  if (d_psrc) cudaFreeAsync(const_cast<void*>(d_psrc), as_stream(stream_));
   cudaStreamSynchronize(as_stream(stream_));
   cudaStreamDestroy(as_stream(stream_));
 }

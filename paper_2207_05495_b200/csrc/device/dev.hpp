@@ -133,8 +133,6 @@ class Context {
 
   // Transition tables in device memory (uploaded once).
   const void* d_img = nullptr;   // u16[k*n]  delta(q,a) at [a*n+q]
-  const void* d_poff = nullptr;  // u16/u32[k*n+1] CSR offsets of the inverse
-  const void* d_psrc = nullptr;  // u16[n*k] CSR sources
   bool timing = false;           // record CUDA-event time of expansion kernels
   bool contain_stats = false;    // count traversal visits / pair tests (one readback per launch)
   Counters counters;

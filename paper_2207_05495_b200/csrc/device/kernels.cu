@@ -22,67 +22,70 @@ namespace synchro::dev {
 
 constexpr int kSliceWarps = 4;
 constexpr size_t kStageSmemLimit = 200 * 1024;
-// Image as a gather over the CSR of delta^-1 (out[t] = OR of the slices of
-// t's sources) instead of shared-memory atomicOr scatters into per-warp
-// output slices.  Measured slower (2^24 parents, n=300: 1.76 vs 2.11 TB/s —
-// the in-degree divergence costs more than the atomics), so off.
-#ifndef SW_IMAGE_GATHER
-#define SW_IMAGE_GATHER 0
-#endif
-constexpr bool kImageGather = SW_IMAGE_GATHER != 0;
 
-// Shared memory of the sliced kernel: per warp 64W input slices (+ 64W output
-// slices for the scatter image), and (STAGED) a 64·k·W-word child block +
-// 64·k cards; then the table (u16 delta, or the CSR of delta^-1).
+// Per-warp slice block: 64W slices (+ pad, keeps 16-byte alignment).
+template <int W>
+constexpr u32 slice_stride() {
+  return 64 * W + 2;
+}
+
+// Shared memory of the sliced kernel: per warp the input slices (+ output
+// slices for the image), and (STAGED) a 64·(kW|1)-word staging block + 64·k
+// cards; then the table (u16 delta).
+//
+// (Measured alternative, dropped: the image as a gather over a per-letter,
+// bank-aware schedule of the inverse (targets in 32-lane groups by
+// in-degree, register accumulators, one store per target) — fewer shared
+// wavefronts than the atomicOr scatter but more instructions and dependent
+// load chains: 0.99 vs 0.86 ms for 2^24 parents at n=300.)
 template <int W>
 static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
-  const bool out_slices = !inverse && !kImageGather;
-  size_t per_warp = (out_slices ? 2 : 1) * 64 * W * sizeof(u64);
-  if (staged) per_warp += static_cast<size_t>(64) * k * (W * sizeof(u64) + sizeof(u32));
-  const size_t kn = static_cast<size_t>(k) * n;
-  const size_t table = (!inverse && kImageGather) ? (kn + 1) * 4 + kn * 2 : kn * 2;
+  size_t per_warp = (inverse ? 1 : 2) * slice_stride<W>() * sizeof(u64);
+  if (staged) per_warp += static_cast<size_t>(64) * ((k * W) | 1) * sizeof(u64) + 64 * k * sizeof(u32);
+  const size_t table = static_cast<size_t>(k) * n * 2;
   return kSliceWarps * per_warp + ((table + 15) & ~size_t{15});
 }
 
-// STAGED: the warp's 64 parents arrive as one contiguous block (coalesced
-// 8-B loads into the staging area), and its 64·k children — contiguous in the
-// output because child o = i·k + a — leave as one block, so every global
-// access is a full-sector coalesced one.  Unstaged (large k·W only): rows are
-// read and written directly by their lanes (8-B accesses at stride 8W / 8kW).
+// STAGED: the warp's 64 parents arrive as one contiguous block and its 64·k
+// children — contiguous in the output because child o = i·k + a — leave as
+// one block, with 16-byte global accesses for full batches (8-byte ones for
+// the tail, or when the slice start leaves the rows 8-byte aligned).  In the
+// staging area rows sit at an ODD stride in words (parents W|1, a parent's k
+// children kW|1), so the lanes' row-strided 8-byte accesses hit 16 distinct
+// bank pairs (2 wavefronts, the minimum).  Unstaged (large k·W only): rows
+// are read and written directly by their lanes.
 template <int W, bool INV, bool STAGED>
 __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
-    const uint16_t* __restrict__ g_img, const u32* __restrict__ g_off,
-    const uint16_t* __restrict__ g_src, u64* __restrict__ out, u32* __restrict__ out_card,
+    const uint16_t* __restrict__ g_img, u64* __restrict__ out, u32* __restrict__ out_card,
     u64* __restrict__ out_tag) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 kn = k * n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // [warps][64W] input slices, [warps][64W] output slices (image),
-  // (STAGED) [warps][64kW] child block, [warps][64k] cards; table u16[k][n]
-  constexpr bool GATHER = !INV && kImageGather;
+  constexpr u32 SP = W | 1;           // staged parent stride (words)
+  constexpr u32 SS = slice_stride<W>();
+  const u32 kW = k * W, CP = kW | 1;  // staged children stride per parent
+  // e / kW == umulhi(e, magic) for the e < 64·kW used here (kW = 1: magic wraps to 0)
+  const u32 magic = 0xFFFFFFFFu / kW + 1;
+  // [warps][SS] input slices, [warps][SS] output slices (image),
+  // (STAGED) [warps][64·CP] staging block, [warps][64k] cards; table u16[k][n]
   u64* s_slices = reinterpret_cast<u64*>(smem);
-  unsigned char* p = smem + ((INV || GATHER) ? 1 : 2) * kSliceWarps * 64 * W * sizeof(u64);
+  unsigned char* p = smem + (INV ? 1 : 2) * kSliceWarps * SS * sizeof(u64);
   u64* stage = nullptr;
   u32* scard = nullptr;
   if (STAGED) {
-    stage = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * 64 * k * W;
-    p += static_cast<size_t>(kSliceWarps) * 64 * k * W * sizeof(u64);
+    stage = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * 64 * CP;
+    p += static_cast<size_t>(kSliceWarps) * 64 * CP * sizeof(u64);
     scard = reinterpret_cast<u32*>(p) + static_cast<size_t>(wid) * 64 * k;
     p += static_cast<size_t>(kSliceWarps) * 64 * k * sizeof(u32);
   }
   uint16_t* s_tab = reinterpret_cast<uint16_t*>(p);
-  u32* s_off = reinterpret_cast<u32*>(p);  // GATHER: CSR offsets, then sources
-  uint16_t* s_src = reinterpret_cast<uint16_t*>(s_off + kn + 1);
-  if (GATHER) {
-    for (u32 i = threadIdx.x; i <= kn; i += blockDim.x) s_off[i] = g_off[i];
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_src[i] = g_src[i];
-  } else {
-    for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
-  }
+  for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
+  u64* sl = s_slices + static_cast<size_t>(wid) * SS;
+  u64* so = INV ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * SS;
   __syncthreads();
-  u64* sl = s_slices + static_cast<size_t>(wid) * 64 * W;
-  u64* so = (INV || GATHER) ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * 64 * W;
+  const bool src16 = ((reinterpret_cast<uintptr_t>(src + lo * W)) & 15) == 0;
+  const bool out16 = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(out_card)) & 15) == 0;
   const u64 batches = (count + 63) / 64;
   for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
@@ -91,7 +94,30 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     const u32 nb = static_cast<u32>(count - b * 64 < 64 ? count - b * 64 : 64);  // parents here
     if (STAGED) {
       const u64* blk = src + (lo + b * 64) * W;
-      for (u32 e = lane; e < 64 * W; e += 32) stage[e] = e < nb * W ? __ldg(blk + e) : 0;
+      if (nb == 64 && src16) {  // 32W 16-byte loads, all issued before any store
+        constexpr int kIt = (32 * W + 31) / 32;
+        uint4 v[kIt];
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+          const u32 e2 = it * 32 + lane;
+          if (e2 < 32 * W) v[it] = __ldg(reinterpret_cast<const uint4*>(blk) + e2);
+        }
+#pragma unroll
+        for (int it = 0; it < kIt; ++it) {
+          const u32 e2 = it * 32 + lane;
+          if (e2 < 32 * W) {
+            const u32 e = 2 * e2, r = e / W, w = e - r * W;
+            stage[r * SP + w] = (static_cast<u64>(v[it].y) << 32) | v[it].x;
+            const u32 r1 = w + 1 == W ? r + 1 : r, w1 = w + 1 == W ? 0 : w + 1;
+            stage[r1 * SP + w1] = (static_cast<u64>(v[it].w) << 32) | v[it].z;
+          }
+        }
+      } else {
+        for (u32 e = lane; e < 64 * W; e += 32) {
+          const u32 r = e / W, w = e - r * W;
+          stage[r * SP + w] = e < nb * W ? __ldg(blk + e) : 0;
+        }
+      }
       __syncwarp();
     }
     // ---- parents -> slices
@@ -99,8 +125,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     for (int w = 0; w < W; ++w) {
       u64 r0, r1;
       if (STAGED) {
-        r0 = stage[lane * W + w];
-        r1 = stage[(lane + 32) * W + w];
+        r0 = stage[lane * SP + w];
+        r1 = stage[(lane + 32) * SP + w];
       } else {
         r0 = v0 ? __ldg(src + (lo + i0) * W + w) : 0;
         r1 = v1 ? __ldg(src + (lo + i1) * W + w) : 0;
@@ -114,7 +140,7 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     for (u32 a = 0; a < k; ++a) {
       const u32 base = a * n;
       u32 card0 = 0, card1 = 0;
-      if (!INV && !GATHER) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
+      if (!INV) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
 #pragma unroll
         for (int i = 0; i < 2 * W; ++i) so[32 * i + lane] = 0;
         __syncwarp();
@@ -133,23 +159,16 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const u32 p = 64 * w + 32 * h + lane;
-          if (INV) {
+          if (INV)
             s[h] = p < n ? sl[s_tab[base + p]] : 0;  // preimage: pure gather
-          } else if (GATHER) {  // image: OR of the slices of p's sources under letter a
-            u64 acc = 0;
-            if (p < n)
-              for (u32 e = s_off[base + p], end = s_off[base + p + 1]; e < end; ++e)
-                acc |= sl[s_src[e]];
-            s[h] = acc;
-          } else {
+          else
             s[h] = so[p];
-          }
         }
         u64 r0, r1;
         transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
         if (STAGED) {
-          stage[(lane * k + a) * W + w] = r0;
-          stage[((lane + 32) * k + a) * W + w] = r1;
+          stage[lane * CP + a * W + w] = r0;
+          stage[(lane + 32) * CP + a * W + w] = r1;
         } else {
           if (v0) out[(i0 * k + a) * W + w] = r0;
           if (v1) out[(i1 * k + a) * W + w] = r1;
@@ -176,14 +195,30 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
       const u64 o0 = b * 64 * k;
       const u32 nc = nb * k;
       u64* dst = out + o0 * W;
-      for (u32 e = lane; e < nc * W; e += 32) dst[e] = stage[e];
-      for (u32 e = lane; e < nc; e += 32) {
-        out_card[o0 + e] = scard[e];
-        if (out_tag) {
+      if (nb == 64 && out16) {  // 16-byte stores (o0·W words is a multiple of 2·64)
+        for (u32 e2 = lane; e2 < 32 * kW; e2 += 32) {
+          const u32 e = 2 * e2, i = kW == 1 ? e : __umulhi(e, magic), off = e - i * kW;
+          const u64 x = stage[i * CP + off];
+          const u64 y = off + 1 == kW ? stage[(i + 1) * CP] : stage[i * CP + off + 1];
+          __stcs(reinterpret_cast<uint4*>(dst) + e2,
+                 make_uint4(static_cast<u32>(x), static_cast<u32>(x >> 32), static_cast<u32>(y),
+                            static_cast<u32>(y >> 32)));
+        }
+        for (u32 e4 = lane; e4 < 16 * k; e4 += 32)
+          __stcs(reinterpret_cast<uint4*>(out_card + o0) + e4,
+                 reinterpret_cast<const uint4*>(scard)[e4]);
+      } else {
+        for (u32 e = lane; e < nc * W; e += 32) {
+          const u32 i = kW == 1 ? e : __umulhi(e, magic), off = e - i * kW;
+          dst[e] = stage[i * CP + off];
+        }
+        for (u32 e = lane; e < nc; e += 32) out_card[o0 + e] = scard[e];
+      }
+      if (out_tag)
+        for (u32 e = lane; e < nc; e += 32) {
           const u64 o = o0 + e;
           out_tag[o] = ((lo + o / k) << 16) | (o % k);
         }
-      }
       __syncwarp();
     }
   }
@@ -214,9 +249,7 @@ void expand(Context& c, const DList& src, size_t lo, size_t hi, bool inverse, DL
                                   : expand_sliced_kernel<W, false, false>);
     if (shmem > 48 * 1024) smem_opt_in(reinterpret_cast<const void*>(kern), static_cast<int>(shmem));
     kern<<<grid, block, shmem, s>>>(src.words, lo, cnt, n, k,
-                                    static_cast<const uint16_t*>(c.d_img),
-                                    static_cast<const u32*>(c.d_poff),
-                                    static_cast<const uint16_t*>(c.d_psrc), out.words, out.cards,
+                                    static_cast<const uint16_t*>(c.d_img), out.words, out.cards,
                                     out.tagged() ? out.tags : nullptr);
   });
   SW_CHECK_LAUNCH();

@@ -68,9 +68,12 @@ __device__ __forceinline__ u64 range_mask(int w, int s, int e) {
 // Stage j pairs lane l with l^j: the lane with bit j clear keeps x & ~m and
 // needs its partner's (x & ~m) >> j; the lane with bit j set keeps x & m and
 // needs (x & m) << j.  So each lane pre-shifts exactly the half its partner
-// needs and ships only that: mask, 32-bit rotate (no bits wrap — the masks
-// are zero where a rotate would wrap), one shuffle, merge = 4 instructions
-// per 32-bit word per stage.
+// needs.  The two halves ship in ONE 32-bit shuffle: the half of `hi` the
+// partner needs is pre-rotated into the positions `keep` frees, the half of
+// `lo` rides unrotated in the other positions (no bits wrap — the masks are
+// zero where a rotate would wrap), and the receiver rotates the lo half
+// home.  One shuffle + 7 ALU ops per stage for 64 bits: shuffles go through
+// the shared-memory pipe, which bounds the bit-sliced kernels.
 __device__ __forceinline__ u32 rotl32(u32 x, u32 r) { return __funnelshift_l(x, x, r); }
 
 __device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
@@ -82,10 +85,12 @@ __device__ __forceinline__ u64 transpose32x2(u64 x, int lane) {
     const bool up = (lane & j) != 0;
     const u32 keep = up ? kM[s] : ~kM[s];
     const u32 rot = up ? 32 - j : j;
-    const u32 sh = __shfl_xor_sync(0xFFFFFFFFu, rotl32(hi & ~keep, rot), j);
-    const u32 sl = __shfl_xor_sync(0xFFFFFFFFu, rotl32(lo & ~keep, rot), j);
-    hi = (hi & keep) | sh;
-    lo = (lo & keep) | sl;
+    // rotl(~keep, rot) == keep for these periodic masks, so each merge is one
+    // rotate + one bit-select (LOP3)
+    const u32 pk = (rotl32(hi, rot) & keep) | (lo & ~keep);
+    const u32 r = __shfl_xor_sync(0xFFFFFFFFu, pk, j);
+    hi = (hi & keep) | (r & ~keep);
+    lo = (lo & keep) | (rotl32(r, 32 - rot) & ~keep);
   }
   return (static_cast<u64>(hi) << 32) | lo;
 }
