@@ -29,9 +29,16 @@ constexpr u32 slice_stride() {
   return 64 * W + 2;
 }
 
-// Shared memory of the sliced kernel: per warp the input slices (+ output
-// slices for the image), and (STAGED) a 64·(kW|1)-word staging block + 64·k
-// cards; then the table (u16 delta).
+// Shared memory of the sliced kernel, per warp: the input slices; STAGED:
+// a staging area + 64·k cards; then the table (u16 delta).  The staging area
+// takes the parents on the way in and the children on the way out, either
+//   rows           64 parents at stride kW|1 words, a parent's k children
+//                  side by side (+ separate output slices for the image), or
+//   letter blocks  (image, W >= 3) k blocks of 64 rows at stride W|1, one
+//                  letter's children each; letter a's output slices live in
+//                  block a until its children overwrite them — 8.2 instead of
+//                  11.3 KB per warp at W=5, k=2 (n=300 image 0.86 -> 0.80 ms,
+//                  n=570 2.43 -> 1.62 ms).
 //
 // (Measured alternative, dropped: the image as a gather over a per-letter,
 // bank-aware schedule of the inverse (targets in 32-lane groups by
@@ -39,9 +46,19 @@ constexpr u32 slice_stride() {
 // wavefronts than the atomicOr scatter but more instructions and dependent
 // load chains: 0.99 vs 0.86 ms for 2^24 parents at n=300.)
 template <int W>
+constexpr bool letter_blocks(bool inverse) {  // measured: W = 2 image and the preimage prefer rows
+  return !inverse && W >= 3;
+}
+
+template <int W>
 static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
-  size_t per_warp = (inverse ? 1 : 2) * slice_stride<W>() * sizeof(u64);
-  if (staged) per_warp += static_cast<size_t>(64) * ((k * W) | 1) * sizeof(u64) + 64 * k * sizeof(u32);
+  size_t per_warp = slice_stride<W>() * sizeof(u64);
+  if (staged)
+    per_warp += (letter_blocks<W>(inverse) ? static_cast<size_t>(k) * (64 * (W | 1) + 4)
+                                           : static_cast<size_t>(64) * ((k * W) | 1)) *
+                    sizeof(u64) +
+                64 * k * sizeof(u32);
+  if (!inverse && !(staged && letter_blocks<W>(inverse))) per_warp += slice_stride<W>() * sizeof(u64);
   const size_t table = static_cast<size_t>(k) * n * 2;
   return kSliceWarps * per_warp + ((table + 15) & ~size_t{15});
 }
@@ -49,50 +66,66 @@ static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
 // STAGED: the warp's 64 parents arrive as one contiguous block and its 64·k
 // children — contiguous in the output because child o = i·k + a — leave as
 // one block, with 16-byte global accesses for full batches (8-byte ones for
-// the tail, or when the slice start leaves the rows 8-byte aligned).  In the
-// staging area rows sit at an ODD stride in words (parents W|1, a parent's k
-// children kW|1), so the lanes' row-strided 8-byte accesses hit 16 distinct
-// bank pairs (2 wavefronts, the minimum).  Unstaged (large k·W only): rows
-// are read and written directly by their lanes.
+// the tail, or when the slice start leaves the rows 8-byte aligned).  Staged
+// rows sit at an ODD stride in words (W|1), so the lanes' row-strided 8-byte
+// accesses hit 16 distinct bank pairs (2 wavefronts, the minimum).
+// Unstaged (large k·W only): rows are read and written directly by lanes.
+// At least six 4-warp blocks per SM (<= 80 registers; image measured 0.86 ->
+// 0.81 ms at n=300 against the unconstrained allocation).
 template <int W, bool INV, bool STAGED>
-__global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
+__global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
     const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
     const uint16_t* __restrict__ g_img, u64* __restrict__ out, u32* __restrict__ out_card,
     u64* __restrict__ out_tag) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 kn = k * n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr u32 SP = W | 1;           // staged parent stride (words)
+  constexpr bool LB = letter_blocks<W>(INV);
+  constexpr u32 SP = W | 1;  // staged parent stride (words)
+  // LB: one letter block; +4 words so the k <= 4 blocks start in different
+  // bank pairs (the output copy reads the same row of two letters side by side)
+  constexpr u32 BLK = 64 * SP + 4;
+  const u32 CP = (k * W) | 1;  // rows: children stride per parent
   constexpr u32 SS = slice_stride<W>();
-  const u32 kW = k * W, CP = kW | 1;  // staged children stride per parent
+  const u32 kW = k * W;
   // e / kW == umulhi(e, magic) for the e < 64·kW used here (kW = 1: magic wraps to 0)
   const u32 magic = 0xFFFFFFFFu / kW + 1;
-  // [warps][SS] input slices, [warps][SS] output slices (image),
-  // (STAGED) [warps][64·CP] staging block, [warps][64k] cards; table u16[k][n]
-  u64* s_slices = reinterpret_cast<u64*>(smem);
-  unsigned char* p = smem + (INV ? 1 : 2) * kSliceWarps * SS * sizeof(u64);
+  u64* sl = reinterpret_cast<u64*>(smem) + static_cast<size_t>(wid) * SS;
+  unsigned char* p = smem + static_cast<size_t>(kSliceWarps) * SS * sizeof(u64);
   u64* stage = nullptr;
   u32* scard = nullptr;
+  u64* so = nullptr;
   if (STAGED) {
-    stage = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * 64 * CP;
-    p += static_cast<size_t>(kSliceWarps) * 64 * CP * sizeof(u64);
+    const u32 area = LB ? k * BLK : 64 * CP;
+    stage = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * area;
+    p += static_cast<size_t>(kSliceWarps) * area * sizeof(u64);
     scard = reinterpret_cast<u32*>(p) + static_cast<size_t>(wid) * 64 * k;
     p += static_cast<size_t>(kSliceWarps) * 64 * k * sizeof(u32);
   }
+  if (!INV && !(STAGED && LB)) {
+    so = reinterpret_cast<u64*>(p) + static_cast<size_t>(wid) * SS;
+    p += static_cast<size_t>(kSliceWarps) * SS * sizeof(u64);
+  }
   uint16_t* s_tab = reinterpret_cast<uint16_t*>(p);
   for (u32 i = threadIdx.x; i < kn; i += blockDim.x) s_tab[i] = g_img[i];
-  u64* sl = s_slices + static_cast<size_t>(wid) * SS;
-  u64* so = INV ? nullptr : s_slices + static_cast<size_t>(kSliceWarps + wid) * SS;
   __syncthreads();
   const bool src16 = ((reinterpret_cast<uintptr_t>(src + lo * W)) & 15) == 0;
   const bool out16 = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(out_card)) & 15) == 0;
+  // staged position of output element e of a batch (child e / W, word e % W)
+  auto child_at = [&](u32 i, u32 rem) {  // child i of the batch, word rem of its kW
+    if (LB) {
+      const u32 a = rem / W;
+      return a * BLK + i * SP + (rem - a * W);
+    }
+    return i * CP + rem;
+  };
   const u64 batches = (count + 63) / 64;
   for (u64 b = static_cast<u64>(blockIdx.x) * kSliceWarps + wid; b < batches;
        b += static_cast<u64>(gridDim.x) * kSliceWarps) {
     const u64 i0 = b * 64 + lane, i1 = i0 + 32;
     const bool v0 = i0 < count, v1 = i1 < count;
     const u32 nb = static_cast<u32>(count - b * 64 < 64 ? count - b * 64 : 64);  // parents here
-    if (STAGED) {
+    if (STAGED) {  // parents into letter block 0
       const u64* blk = src + (lo + b * 64) * W;
       if (nb == 64 && src16) {  // 32W 16-byte loads, all issued before any store
         constexpr int kIt = (32 * W + 31) / 32;
@@ -139,34 +172,45 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
     __syncwarp();
     for (u32 a = 0; a < k; ++a) {
       const u32 base = a * n;
-      u32 card0 = 0, card1 = 0;
-      if (!INV) {  // image: scatter the slices, so[delta(q,a)] |= sl[q] (smem atomics)
+      u64* blk = STAGED && LB ? stage + a * BLK : nullptr;
+      u64 s[W][2];  // image: this letter's output slices (dead code for the preimage)
+      if (!INV) {  // image: scatter the slices, o[delta(q,a)] |= sl[q] (smem atomics)
+        u64* o = STAGED && LB ? blk : so;
 #pragma unroll
-        for (int i = 0; i < 2 * W; ++i) so[32 * i + lane] = 0;
+        for (int i = 0; i < 2 * W; ++i) o[32 * i + lane] = 0;
         __syncwarp();
         // two native 32-bit ORs (a 64-bit shared atomicOr is a CAS spin loop)
         for (u32 q = lane; q < n; q += 32) {
           const u64 v = sl[q];
-          u32* dst = reinterpret_cast<u32*>(&so[s_tab[base + q]]);
+          u32* dst = reinterpret_cast<u32*>(&o[s_tab[base + q]]);
           if (static_cast<u32>(v)) atomicOr(dst, static_cast<u32>(v));
           if (v >> 32) atomicOr(dst + 1, static_cast<u32>(v >> 32));
         }
         __syncwarp();
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) s[w][h] = o[64 * w + 32 * h + lane];
+        __syncwarp();  // block a now takes this letter's children
       }
+      u32 card0 = 0, card1 = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        u64 s[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const u32 p = 64 * w + 32 * h + lane;
-          if (INV)
-            s[h] = p < n ? sl[s_tab[base + p]] : 0;  // preimage: pure gather
-          else
-            s[h] = so[p];
+        u64 x0, x1;
+        if constexpr (INV) {  // preimage: pure gather
+          const u32 q0 = 64 * w + lane, q1 = q0 + 32;
+          x0 = q0 < n ? sl[s_tab[base + q0]] : 0;
+          x1 = q1 < n ? sl[s_tab[base + q1]] : 0;
+        } else {
+          x0 = s[w][0];
+          x1 = s[w][1];
         }
         u64 r0, r1;
-        transpose64(s[0], s[1], lane, r0, r1);  // child rows i0, i1 — word w
-        if (STAGED) {
+        transpose64(x0, x1, lane, r0, r1);  // child rows i0, i1 — word w
+        if (STAGED && LB) {
+          blk[lane * SP + w] = r0;
+          blk[(lane + 32) * SP + w] = r1;
+        } else if (STAGED) {
           stage[lane * CP + a * W + w] = r0;
           stage[(lane + 32) * CP + a * W + w] = r1;
         } else {
@@ -196,10 +240,23 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
       const u32 nc = nb * k;
       u64* dst = out + o0 * W;
       if (nb == 64 && out16) {  // 16-byte stores (o0·W words is a multiple of 2·64)
+        // element 2·e2 = child i, word rem of its k·W; lanes advance by 64
+        // elements (di children + dr words) per iteration
+        const u32 di = 64 / kW, dr = 64 - di * kW;
+        u32 i = kW == 1 ? 2 * lane : __umulhi(2 * lane, magic), rem = 2 * lane - i * kW;
         for (u32 e2 = lane; e2 < 32 * kW; e2 += 32) {
-          const u32 e = 2 * e2, i = kW == 1 ? e : __umulhi(e, magic), off = e - i * kW;
-          const u64 x = stage[i * CP + off];
-          const u64 y = off + 1 == kW ? stage[(i + 1) * CP] : stage[i * CP + off + 1];
+          u32 i1 = i, r1 = rem + 1;
+          if (r1 == kW) {
+            r1 = 0;
+            ++i1;
+          }
+          const u64 x = stage[child_at(i, rem)], y = stage[child_at(i1, r1)];
+          i += di;
+          rem += dr;
+          if (rem >= kW) {
+            rem -= kW;
+            ++i;
+          }
           __stcs(reinterpret_cast<uint4*>(dst) + e2,
                  make_uint4(static_cast<u32>(x), static_cast<u32>(x >> 32), static_cast<u32>(y),
                             static_cast<u32>(y >> 32)));
@@ -209,8 +266,8 @@ __global__ void __launch_bounds__(kSliceWarps * 32) expand_sliced_kernel(
                  reinterpret_cast<const uint4*>(scard)[e4]);
       } else {
         for (u32 e = lane; e < nc * W; e += 32) {
-          const u32 i = kW == 1 ? e : __umulhi(e, magic), off = e - i * kW;
-          dst[e] = stage[i * CP + off];
+          const u32 i = kW == 1 ? e : __umulhi(e, magic);
+          dst[e] = stage[child_at(i, e - i * kW)];
         }
         for (u32 e = lane; e < nc; e += 32) out_card[o0 + e] = scard[e];
       }
