@@ -80,6 +80,8 @@ Context::~Context() {
   cudaSetDevice(device_);
   for (auto& s : scratch_)
     if (s.p) cudaFreeAsync(s.p, as_stream(stream_));
+  for (auto& v : cache_)
+    for (void* p : v) cudaFreeAsync(p, as_stream(stream_));
   if (d_img) cudaFreeAsync(const_cast<void*>(d_img), as_stream(stream_));
   cudaStreamSynchronize(as_stream(stream_));
   cudaStreamDestroy(as_stream(stream_));
@@ -87,13 +89,38 @@ Context::~Context() {
 
 void* Context::alloc(size_t bytes) {
   if (bytes == 0) bytes = 16;
+  int cls = -1;
+  if (bytes <= (size_t{256} << (kCacheClasses - 1))) {
+    cls = 0;
+    while ((size_t{256} << cls) < bytes) ++cls;
+    if (!cache_[cls].empty()) {
+      void* p = cache_[cls].back();
+      cache_[cls].pop_back();
+      cached_bytes_ -= size_t{256} << cls;
+      cached_live_[p] = cls;
+      return p;
+    }
+    bytes = size_t{256} << cls;
+  }
   void* p = nullptr;
   SW_CUDA(cudaMallocFromPoolAsync(&p, bytes, static_cast<cudaMemPool_t>(pool_), as_stream(stream_)));
+  if (cls >= 0) cached_live_[p] = cls;
   return p;
 }
 
 void Context::free(void* p) {
-  if (p) SW_CUDA(cudaFreeAsync(p, as_stream(stream_)));
+  if (!p) return;
+  constexpr size_t kMaxCached = size_t{256} << 20;
+  if (auto it = cached_live_.find(p); it != cached_live_.end()) {
+    const int cls = it->second;
+    cached_live_.erase(it);
+    if (cached_bytes_ + (size_t{256} << cls) <= kMaxCached) {
+      cache_[cls].push_back(p);
+      cached_bytes_ += size_t{256} << cls;
+      return;
+    }
+  }
+  SW_CUDA(cudaFreeAsync(p, as_stream(stream_)));
 }
 
 void Context::memcpy_d2d(void* dst, const void* src, size_t bytes) {
@@ -122,9 +149,25 @@ double StreamTimer::stop_ms() {
   return ms;
 }
 
+// Small readbacks (sizes, flags, counters: several per engine step) go
+// through a pinned staging buffer: a device-to-pageable copy is staged by the
+// driver under a lock that the batch runner's threads contend on.
+constexpr size_t kPinnedBytes = 64 * 1024;
+
 void Context::memcpy_d2h(void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   counters.d2h_bytes += bytes;
+  if (bytes <= kPinnedBytes) {
+    // one buffer per host thread, kept for the thread's lifetime (allocating
+    // and freeing pinned memory per context costs milliseconds: cudaFreeHost
+    // synchronises the device)
+    thread_local void* pinned = nullptr;
+    if (!pinned) SW_CUDA(cudaHostAlloc(&pinned, kPinnedBytes, cudaHostAllocPortable));
+    SW_CUDA(cudaMemcpyAsync(pinned, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream_)));
+    sync();
+    std::memcpy(dst, pinned, bytes);
+    return;
+  }
   SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream_)));
   sync();
 }

@@ -13,6 +13,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <unordered_map>
 #include <vector>
 
 #include "../automaton.hpp"
@@ -145,6 +146,14 @@ class Context {
   int device_ = 0;
   void* stream_ = nullptr;
   void* pool_ = nullptr;  // cudaMemPool_t (the device's default pool)
+  // Host-side cache of small freed blocks by power-of-two class (256 B ..
+  // 4 MB): small solves allocate and free hundreds of lists, and every pool
+  // call takes a driver lock the batch runner's threads contend on.  One
+  // stream per context, so a block freed here is reusable at once.
+  static constexpr int kCacheClasses = 15;
+  std::vector<void*> cache_[kCacheClasses];
+  std::unordered_map<void*, int> cached_live_;
+  size_t cached_bytes_ = 0;
   struct Scratch { void* p = nullptr; size_t bytes = 0; };
   Scratch scratch_[11];  // slots: kernels.cuh
 };

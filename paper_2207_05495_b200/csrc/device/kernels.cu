@@ -401,6 +401,10 @@ struct StatsAcc {
   unsigned int max;
 };
 
+// DIRECT (one block): the block's result is the answer — no accumulator
+// initialisation copy before the launch (small lists: config-2 solves refresh
+// stats several times per step).
+template <bool DIRECT>
 __global__ void stats_kernel(const u32* cards, u64 count, StatsAcc* acc) {
   u64 sum = 0;
   u32 mn = 0xFFFFFFFFu, mx = 0;
@@ -421,9 +425,13 @@ __global__ void stats_kernel(const u32* cards, u64 count, StatsAcc* acc) {
   __syncthreads();
   const u32 bmx = BR32(t2).Reduce(mx, cub::Max());
   if (threadIdx.x == 0) {
-    atomicAdd(&acc->sum, static_cast<unsigned long long>(bs));
-    atomicMin(&acc->min, bmn);
-    atomicMax(&acc->max, bmx);
+    if (DIRECT) {
+      *acc = StatsAcc{static_cast<unsigned long long>(bs), bmn, bmx};
+    } else {
+      atomicAdd(&acc->sum, static_cast<unsigned long long>(bs));
+      atomicMin(&acc->min, bmn);
+      atomicMax(&acc->max, bmx);
+    }
   }
 }
 
@@ -433,8 +441,13 @@ ListStats stats(Context& c, const DList& l) {
   if (l.empty()) return st;
   StatsAcc h{0, 0xFFFFFFFFu, 0};
   auto* d = static_cast<StatsAcc*>(c.scratch(7, sizeof(StatsAcc)));
-  c.memcpy_h2d(d, &h, sizeof(h));
-  stats_kernel<<<grid_for(l.size(), 256, 148 * 4), 256, 0, as_stream(c.stream())>>>(l.cards, l.size(), d);
+  if (l.size() <= 256 * 64) {
+    stats_kernel<true><<<1, 256, 0, as_stream(c.stream())>>>(l.cards, l.size(), d);
+  } else {
+    c.memcpy_h2d(d, &h, sizeof(h));
+    stats_kernel<false><<<grid_for(l.size(), 256, 148 * 4), 256, 0, as_stream(c.stream())>>>(
+        l.cards, l.size(), d);
+  }
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches++;
   c.memcpy_d2h(&h, d, sizeof(h));
@@ -538,10 +551,71 @@ struct KeepUniqueSorted {  // first of each run of equal rows in perm order
   }
 };
 
+// Small lists: the whole compaction in ONE block (tiles of 1024 in order,
+// carry in shared memory) into an output sized for every row, the total
+// written to *total — one launch instead of three.
+template <int W, class Keep>
+__global__ void __launch_bounds__(1024) compact_small_kernel(
+    u64 count, Keep keep, const u32* __restrict__ perm, const u64* __restrict__ sw,
+    const u32* __restrict__ sc, const u64* __restrict__ st, u64* __restrict__ dw,
+    u32* __restrict__ dc, u64* __restrict__ dt, u32* total) {
+  __shared__ u32 warp_off[32];
+  __shared__ u32 carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (u64 base = 0; base < count; base += 1024) {
+    const u64 i = base + threadIdx.x;
+    const bool f = i < count && keep(i);
+    const unsigned ballot = __ballot_sync(0xFFFFFFFFu, f);
+    if (lane == 0) warp_off[warp] = __popc(ballot);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 32 warp counts
+      const u32 v = warp_off[lane];
+      u32 x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+        if (lane >= d) x += y;
+      }
+      warp_off[lane] = x - v;
+    }
+    __syncthreads();
+    if (f) {
+      const u64 pos = carry + warp_off[warp] + __popc(ballot & ((1u << lane) - 1));
+      const u64 from = perm ? perm[i] : i;
+#pragma unroll
+      for (int w = 0; w < W; ++w) dw[pos * W + w] = sw[from * W + w];
+      dc[pos] = sc[from];
+      if (dt) dt[pos] = st[from];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += warp_off[31] + __popc(ballot);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+constexpr u64 kCompactSmall = 32 * 1024;
+
 template <int W, class Keep>
 static size_t run_compact(Context& c, DList& l, Keep keep, const u32* perm) {
   const u64 count = l.size();
   if (count == 0) return 0;
+  if (count <= kCompactSmall) {
+    auto* tot = static_cast<u32*>(c.scratch(6, sizeof(u32)));
+    DList out(&c, count, l.tagged());
+    compact_small_kernel<W><<<1, 1024, 0, as_stream(c.stream())>>>(
+        count, keep, perm, l.words, l.cards, l.tags, out.words, out.cards,
+        l.tagged() ? out.tags : nullptr, tot);
+    SW_CHECK_LAUNCH();
+    c.counters.kernel_launches += 1;
+    u32 total = 0;
+    c.memcpy_d2h(&total, tot, 4);
+    out.set_size(total);
+    l = std::move(out);
+    return total;
+  }
   const u32 ntiles = static_cast<u32>((count + kTile - 1) / kTile);
   auto* tiles = static_cast<u32*>(c.scratch(6, (ntiles + 1) * sizeof(u32)));
   cudaStream_t s = as_stream(c.stream());
