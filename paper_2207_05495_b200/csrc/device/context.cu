@@ -1,6 +1,11 @@
 // Device context: stream, stream-ordered memory pool, transition tables,
 // list allocation and host<->device transfer.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+
+#include <dlfcn.h>
+#include <execinfo.h>
 #include <sstream>
 #include <vector>
 
@@ -103,6 +108,7 @@ void* Context::alloc(size_t bytes) {
     bytes = size_t{256} << cls;
   }
   void* p = nullptr;
+  counters.allocs++;
   SW_CUDA(cudaMallocFromPoolAsync(&p, bytes, static_cast<cudaMemPool_t>(pool_), as_stream(stream_)));
   if (cls >= 0) cached_live_[p] = cls;
   return p;
@@ -127,7 +133,26 @@ void Context::memcpy_d2d(void* dst, const void* src, size_t bytes) {
   if (bytes) SW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream_)));
 }
 
-void Context::sync() { SW_CUDA(cudaStreamSynchronize(as_stream(stream_))); }
+void Context::sync() {
+  counters.syncs++;
+  static const bool trace = [] {
+    const char* e = std::getenv("SYNCHRO_TRACE_SYNCS");
+    return e && *e == '1';
+  }();
+  if (trace) {  // library offsets of the calling frames (resolve with addr2line)
+    void* fr[6];
+    const int nf = backtrace(fr, 6);
+    std::fprintf(stderr, "SYNC");
+    for (int i = 1; i < nf; ++i) {
+      Dl_info info{};
+      if (dladdr(fr[i], &info) && info.dli_fbase)
+        std::fprintf(stderr, " %zx", static_cast<size_t>(static_cast<char*>(fr[i]) -
+                                                         static_cast<char*>(info.dli_fbase)));
+    }
+    std::fprintf(stderr, "\n");
+  }
+  SW_CUDA(cudaStreamSynchronize(as_stream(stream_)));
+}
 
 StreamTimer::StreamTimer(Context& c) : c_(c) {
   cudaEvent_t a, b;
@@ -203,6 +228,9 @@ DList& DList::operator=(DList&& o) noexcept {
     size_ = o.size_;
     cap_ = o.cap_;
     tagged_ = o.tagged_;
+    stats_ok_ = o.stats_ok_;
+    known_stats_ = o.known_stats_;
+    o.stats_ok_ = false;
     o.words = nullptr;
     o.cards = nullptr;
     o.tags = nullptr;

@@ -23,6 +23,12 @@ namespace synchro::dev {
 
 class Context;
 
+struct ListStats {
+  u64 sum_cards = 0;
+  u32 min_card = 0;  // n for an empty list (set_list.hpp:182-186)
+  u32 max_card = 0;
+};
+
 // Owning device list.  Move-only; memory is stream-ordered (cudaMallocAsync)
 // on the owning context's stream.
 class DList {
@@ -40,7 +46,21 @@ class DList {
   size_t size() const { return size_; }
   bool empty() const { return size_ == 0; }
   bool tagged() const { return tagged_; }
-  void set_size(size_t s) { size_ = s; }
+  void set_size(size_t s) {
+    size_ = s;
+    stats_ok_ = false;
+  }
+  // Card statistics computed as a by-product (small-list compaction), handed
+  // to the next stats() call; cleared by anything that changes size or cards.
+  void set_known_stats(const ListStats& st) {
+    known_stats_ = st;
+    stats_ok_ = true;
+  }
+  bool known_stats(ListStats* st) const {
+    if (stats_ok_) *st = known_stats_;
+    return stats_ok_;
+  }
+  void forget_stats() { stats_ok_ = false; }
 
   u64* words = nullptr;
   u32* cards = nullptr;
@@ -51,13 +71,9 @@ class DList {
   size_t size_ = 0;
   size_t cap_ = 0;
   bool tagged_ = false;
+  bool stats_ok_ = false;
+  ListStats known_stats_;
   friend class Context;
-};
-
-struct ListStats {
-  u64 sum_cards = 0;
-  u32 min_card = 0;  // n for an empty list (set_list.hpp:182-186)
-  u32 max_card = 0;
 };
 
 struct Witness {
@@ -89,6 +105,8 @@ struct Counters {
   u64 contain_pair_tests = 0;
   u64 h2d_bytes = 0;
   u64 d2h_bytes = 0;
+  u64 syncs = 0;           // host waits on the stream (readbacks included)
+  u64 allocs = 0;          // device allocations that reached the memory pool
   double contain_ms = 0;   // CUDA-event time of the traversal kernel (when timed)
   u64 contain_launches = 0;
   u64 contain_bytes = 0;   // algorithmic bytes of those launches

@@ -385,6 +385,7 @@ __global__ void complement_kernel(u64* words, u32* cards, u64 count, u32 n) {
 }
 
 void complement(Context& c, DList& l) {
+  l.forget_stats();
   if (l.empty()) return;
   SW_DISPATCH_W(c.W(), {
     complement_kernel<W><<<grid_for(l.size(), 256), 256, 0, as_stream(c.stream())>>>(
@@ -439,6 +440,7 @@ ListStats stats(Context& c, const DList& l) {
   ListStats st;
   st.min_card = c.n();
   if (l.empty()) return st;
+  if (l.known_stats(&st)) return st;
   StatsAcc h{0, 0xFFFFFFFFu, 0};
   auto* d = static_cast<StatsAcc*>(c.scratch(7, sizeof(StatsAcc)));
   if (l.size() <= 256 * 64) {
@@ -552,17 +554,30 @@ struct KeepUniqueSorted {  // first of each run of equal rows in perm order
 };
 
 // Small lists: the whole compaction in ONE block (tiles of 1024 in order,
-// carry in shared memory) into an output sized for every row, the total
-// written to *total — one launch instead of three.
+// carry in shared memory) into an output sized for every row; the survivor
+// count and the survivors' card statistics come back in ONE readback (the
+// engine refreshes a list's statistics right after compacting it) — one
+// launch and one host wait instead of three launches and two waits.
+struct CompactResult {
+  unsigned long long sum;
+  u32 min, max, count, pad;
+};
+
 template <int W, class Keep>
 __global__ void __launch_bounds__(1024) compact_small_kernel(
     u64 count, Keep keep, const u32* __restrict__ perm, const u64* __restrict__ sw,
     const u32* __restrict__ sc, const u64* __restrict__ st, u64* __restrict__ dw,
-    u32* __restrict__ dc, u64* __restrict__ dt, u32* total) {
+    u32* __restrict__ dc, u64* __restrict__ dt, CompactResult* res) {
   __shared__ u32 warp_off[32];
   __shared__ u32 carry;
+  __shared__ CompactResult acc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    acc = CompactResult{0, 0xFFFFFFFFu, 0, 0, 0};
+  }
+  u64 sum = 0;
+  u32 mn = 0xFFFFFFFFu, mx = 0;
   __syncthreads();
   for (u64 base = 0; base < count; base += 1024) {
     const u64 i = base + threadIdx.x;
@@ -586,14 +601,25 @@ __global__ void __launch_bounds__(1024) compact_small_kernel(
       const u64 from = perm ? perm[i] : i;
 #pragma unroll
       for (int w = 0; w < W; ++w) dw[pos * W + w] = sw[from * W + w];
-      dc[pos] = sc[from];
+      const u32 cd = sc[from];
+      dc[pos] = cd;
       if (dt) dt[pos] = st[from];
+      sum += cd;
+      mn = min(mn, cd);
+      mx = max(mx, cd);
     }
     __syncthreads();
     if (threadIdx.x == 1023) carry += warp_off[31] + __popc(ballot);
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (sum) atomicAdd(&acc.sum, static_cast<unsigned long long>(sum));
+  if (mn != 0xFFFFFFFFu) atomicMin(&acc.min, mn);
+  if (mx) atomicMax(&acc.max, mx);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    acc.count = carry;
+    *res = acc;
+  }
 }
 
 constexpr u64 kCompactSmall = 32 * 1024;
@@ -603,18 +629,23 @@ static size_t run_compact(Context& c, DList& l, Keep keep, const u32* perm) {
   const u64 count = l.size();
   if (count == 0) return 0;
   if (count <= kCompactSmall) {
-    auto* tot = static_cast<u32*>(c.scratch(6, sizeof(u32)));
+    auto* dres = static_cast<CompactResult*>(c.scratch(6, sizeof(CompactResult)));
     DList out(&c, count, l.tagged());
     compact_small_kernel<W><<<1, 1024, 0, as_stream(c.stream())>>>(
         count, keep, perm, l.words, l.cards, l.tags, out.words, out.cards,
-        l.tagged() ? out.tags : nullptr, tot);
+        l.tagged() ? out.tags : nullptr, dres);
     SW_CHECK_LAUNCH();
     c.counters.kernel_launches += 1;
-    u32 total = 0;
-    c.memcpy_d2h(&total, tot, 4);
-    out.set_size(total);
+    CompactResult h{};
+    c.memcpy_d2h(&h, dres, sizeof(h));
+    out.set_size(h.count);
+    ListStats st;
+    st.sum_cards = h.sum;
+    st.min_card = h.count ? h.min : c.n();
+    st.max_card = h.count ? h.max : 0;
+    out.set_known_stats(st);
     l = std::move(out);
-    return total;
+    return h.count;
   }
   const u32 ntiles = static_cast<u32>((count + kTile - 1) / kTile);
   auto* tiles = static_cast<u32*>(c.scratch(6, (ntiles + 1) * sizeof(u32)));

@@ -983,6 +983,10 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
     res.contain_bytes = ctx.counters.contain_bytes;
     res.contain_visits = ctx.counters.contain_visits;
     res.contain_pairs = ctx.counters.contain_pairs;
+    SYNCHRO_PROGRESS("host-device traffic: %llu launches, %llu syncs, %llu pool allocations",
+                     static_cast<unsigned long long>(ctx.counters.kernel_launches),
+                     static_cast<unsigned long long>(ctx.counters.syncs),
+                     static_cast<unsigned long long>(ctx.counters.allocs));
     return res;
   };
 
