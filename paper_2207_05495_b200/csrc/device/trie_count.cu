@@ -26,6 +26,7 @@ namespace synchro::dev {
 namespace {
 
 constexpr u32 kInvalid = 0xFFFFFFFFu;
+constexpr u32 kCountSmall = 16384;  // count-only builds up to this size: one block
 
 struct Seg {
   u32 lo, hi;
@@ -212,6 +213,121 @@ __global__ void init_kernel(u32* idx, u32* seg, u32 N) {
   }
 }
 
+// Count-only construction of a SMALL list in one block: the rounds of
+// hist/pick/scatter above as phases separated by block barriers, the round's
+// segment count in shared memory — one launch and one readback instead of ~4
+// memsets, 3 launches and a readback per trie level (config-2 solves take the
+// ledger's trie count at every DFS start).  Same arithmetic, same count.
+template <int W>
+__global__ void __launch_bounds__(1024) count_small_kernel(
+    const u64* __restrict__ words, u32 N, u32 n, u32 min_leaf, u32* idx, u32* seg, u32* idx2,
+    u32* seg2, Seg* segs, Seg* nsegs, u32* per, u32 max_segs, u32* hist,
+    unsigned long long* nodes_out) {
+  __shared__ u32 nact, next_count;
+  __shared__ unsigned long long nodes;
+  const u32 tid = threadIdx.x, nthr = blockDim.x;
+  for (u32 i = tid; i < N; i += nthr) {
+    idx[i] = i;
+    seg[i] = 0;
+  }
+  if (tid == 0) {
+    segs[0] = Seg{0, N};
+    nact = 1;
+    nodes = 1;
+  }
+  __syncthreads();
+  u32* div = per;
+  u32* zc = per + max_segs;
+  u32* cz = per + 2 * max_segs;
+  u32* co = per + 3 * max_segs;
+  u32* curz = per + 4 * max_segs;
+  u32* curo = per + 5 * max_segs;
+  while (nact > 0) {
+    const u32 na = nact;
+    for (u32 i = tid; i < na * n; i += nthr) hist[i] = 0;
+    for (u32 i = tid; i < na; i += nthr) curz[i] = curo[i] = 0;
+    if (tid == 0) next_count = 0;
+    __syncthreads();
+    for (u32 i = tid; i < N; i += nthr) {  // per-segment state histograms
+      const u32 sg = seg[i];
+      if (sg == kInvalid) continue;
+      const u64* x = words + static_cast<u64>(idx[i]) * W;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        u64 bits = x[w];
+        while (bits) {
+          const int b = __clzll(bits);
+          bits &= ~(u64{1} << (63 - b));
+          atomicAdd(&hist[sg * n + w * 64 + b], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    const u32 lane = tid & 31;
+    for (u32 wp = tid >> 5; wp < na; wp += nthr >> 5) {  // one warp per segment: division state
+      const Seg sg = segs[wp];
+      const u32 total = sg.hi - sg.lo;
+      u32 best_c = 0, best_q = kInvalid;
+      for (u32 q = lane; q < n; q += 32) {
+        const u32 v = hist[wp * n + q];
+        if (v < total && v > best_c) {
+          best_c = v;
+          best_q = q;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        const u32 oc = __shfl_xor_sync(0xFFFFFFFFu, best_c, off);
+        const u32 oq = __shfl_xor_sync(0xFFFFFFFFu, best_q, off);
+        if (oc > best_c || (oc == best_c && oq < best_q)) {
+          best_c = oc;
+          best_q = oq;
+        }
+      }
+      if (lane == 0) {
+        div[wp] = best_q;
+        const u32 ones = best_c, zeros = total - ones;
+        zc[wp] = zeros;
+        unsigned long long made = 1;
+        u32 z = kInvalid, o = kInvalid;
+        if (zeros > min_leaf) {
+          ++made;
+          z = atomicAdd(&next_count, 1u);
+          nsegs[z] = Seg{sg.lo, sg.lo + zeros};
+        }
+        if (ones > min_leaf) {
+          o = atomicAdd(&next_count, 1u);
+          nsegs[o] = Seg{sg.lo + zeros, sg.hi};
+        }
+        cz[wp] = z;
+        co[wp] = o;
+        atomicAdd(&nodes, made);
+      }
+    }
+    __syncthreads();
+    for (u32 i = tid; i < N; i += nthr) {  // elements to their child ranges
+      const u32 sg = seg[i];
+      if (sg == kInvalid) {
+        seg2[i] = kInvalid;
+        idx2[i] = idx[i];
+        continue;
+      }
+      const u32 x = div[sg], e = idx[i];
+      const bool one = (words[static_cast<u64>(e) * W + (x >> 6)] >> (63 - (x & 63))) & 1;
+      const u32 r = atomicAdd(one ? &curo[sg] : &curz[sg], 1u);
+      const u32 pos = segs[sg].lo + (one ? zc[sg] : 0) + r;
+      idx2[pos] = e;
+      seg2[pos] = one ? co[sg] : cz[sg];
+    }
+    __syncthreads();
+    u32* t = idx; idx = idx2; idx2 = t;
+    t = seg; seg = seg2; seg2 = t;
+    Seg* ts = segs; segs = nsegs; nsegs = ts;
+    if (tid == 0) nact = next_count;
+    __syncthreads();
+  }
+  if (tid == 0) *nodes_out = nodes;
+}
+
 }  // namespace
 
 // Builds the trie level by level; returns the node count and, with `shape`,
@@ -244,6 +360,30 @@ static u64 build_trie(Context& c, const DList& l, u32 min_leaf, TrieShape* shape
   }
   const u32 N = static_cast<u32>(N64), n = c.n();
   cudaStream_t s = as_stream(c.stream());
+  if (!shape && !qi && N <= kCountSmall) {
+    const u32 max_segs = N / (min_leaf + 1) + 2;
+    u32* buf = static_cast<u32*>(c.alloc((4ull * N + 4ull * max_segs + 6ull * max_segs +
+                                          static_cast<u64>(max_segs) * n + 2) * 4));
+    u32* idx = buf;
+    u32* seg = idx + N;
+    u32* idx2 = seg + N;
+    u32* seg2 = idx2 + N;
+    Seg* segs = reinterpret_cast<Seg*>(seg2 + N);
+    Seg* nsegs = segs + max_segs;
+    u32* per = reinterpret_cast<u32*>(nsegs + max_segs);
+    u32* hist = per + 6ull * max_segs;
+    auto* out = static_cast<unsigned long long*>(c.scratch(7, 8));
+    SW_DISPATCH_W(c.W(), {
+      count_small_kernel<W><<<1, 1024, 0, s>>>(l.words, N, n, min_leaf, idx, seg, idx2, seg2, segs,
+                                               nsegs, per, max_segs, hist, out);
+    });
+    SW_CHECK_LAUNCH();
+    c.counters.kernel_launches += 1;
+    unsigned long long nodes = 0;
+    c.memcpy_d2h(&nodes, out, 8);
+    c.free(buf);
+    return nodes;
+  }
   u32* idx = static_cast<u32*>(c.alloc(N * 4ull));
   u32* seg = static_cast<u32*>(c.alloc(N * 4ull));
   u32* idx2 = static_cast<u32*>(c.alloc(N * 4ull));
