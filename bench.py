@@ -389,6 +389,7 @@ def run_ours(args, world, rank, local):
                             "bytes_per_unit": exp_bytes_per_child,
                             "ms_per_launch": mb_exp_ms, "children_per_launch": mb_count * aut.k,
                             "traffic": traffic["expand"],
+                            "traffic_preimage": traffic["expand_preimage"],
                             "algorithmic_bytes_per_launch": mb_count * aut.k * exp_bytes_per_child,
                             "in_engine_achieved": achieved,
                             "in_engine_share_of_step": exp_ms / engine_ms if engine_ms else None},
@@ -429,7 +430,8 @@ def dram_traffic(W, cont_bytes_per_solve):
     path = os.path.join(ROOT, "profiles", "r02_dram_traffic.json")
     if not os.path.exists(path):
         path = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
-    out = {"contain": None, "contain_note": None, "expand": None, "dedupe": None}
+    out = {"contain": None, "contain_note": None, "expand": None, "expand_preimage": None,
+           "dedupe": None}
     if not os.path.exists(path):
         return out
     t = json.load(open(path))
@@ -444,9 +446,11 @@ def dram_traffic(W, cont_bytes_per_solve):
                                f"({cont[0]['source']}); algorithmic bytes per launch "
                                f"{cont_bytes_per_solve / launches:.3g}")
     for key, name in (("expand", f"expand_sliced_kernel<{W}, 0, 1>"),
-                      ("dedupe", f"unnamed>::dd_single_kernel<{W}>")):
-        if name in t:
-            out[key] = t[name]["traffic_bytes_per_launch"]
+                      ("expand_preimage", f"expand_sliced_kernel<{W}, 1, 1>"),
+                      ("dedupe", f"dd_single_kernel<{W}")):
+        hit = [v for k, v in t.items() if name in k]
+        if hit:
+            out[key] = hit[0]["traffic_bytes_per_launch"]
     return out
 
 

@@ -29,7 +29,16 @@ ncu --set full --import-source on --clock-control none -k regex:"trie_pool_kerne
 ncu --set full --import-source on --clock-control none -k regex:"contain_pool_kernel" \
     --launch-skip $((NM - 1)) --launch-count 1 -o $O/ncu_contain_mark \
     python scripts/one_solve.py random:300,2,0 44 > /dev/null 2>&1
-for r in ncu_trie_exist ncu_contain_mark; do python scripts/ncu_summary.py $O/$r.ncu-rep > $O/$r.txt; done
+# north-star kernels at HBM scale (2^24 parents / rows, n=300): one launch each
+for m in img pre dedupe; do
+  K=expand_sliced; [ $m = dedupe ] && K=dd_single
+  ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip 1 --launch-count 1 \
+      -o $O/ncu_micro_$m python scripts/micro_one.py $m > /dev/null 2>&1
+done
+for r in ncu_trie_exist ncu_contain_mark ncu_micro_img ncu_micro_pre ncu_micro_dedupe; do
+  python scripts/ncu_summary.py $O/$r.ncu-rep > $O/$r.txt
+done
 python scripts/baselines.py $O/baselines.json --skip-full > $O/baselines.log 2>&1
 gzip -f $O/launches.csv $O/traffic_contain.csv $O/traffic_micro.csv
+rm -f $O/*.ncu-rep  # summaries kept (gpurun copies back at most 64 MiB)
 ls -la $O
