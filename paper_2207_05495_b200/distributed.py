@@ -1,4 +1,14 @@
-"""Multi-GPU exact solve: DFS-phase partitioning, one process per GPU.
+"""Multi-GPU exact solve, one process per GPU.
+
+Two modes:
+
+* `solve_exact_partitioned` (the north_star path, `sw_solve_exact_dist`): ONE solve
+  partitioned by hash ownership of each subset — per level an all-to-all carries new
+  subsets to their owner rank, which deduplicates them; containment runs against
+  all-gathered lists; list statistics are all-reduced; the DFS runs interleaved shares
+  with a MIN all-reduce.  Transport: NCCL (`make_comm("nccl")`) or
+  host callbacks over a torch.distributed group (`make_comm("callback", group)`).
+* `solve_exact_sharded` (DFS-phase sharding only, below):
 
 Every rank runs phase 1 (the list steps are deterministic, so all ranks hold
 identical L_BFS / L_IBFS and write identical trace prefixes), then explores
