@@ -29,8 +29,10 @@ constexpr u32 slice_stride() {
   return 64 * W + 2;
 }
 
-// Shared memory of the sliced kernel, per warp: the input slices; STAGED:
-// a staging area + 64·k cards; then the table (u16 delta).  The staging area
+// Shared memory of the sliced kernel, per warp: the input slices (preimage,
+// and the image at W > 6 — below that lane l scatters the slices 64w + l and
+// 64w + 32 + l it already holds from its transposes, straight from registers);
+// STAGED: a staging area + 64·k cards; then the table (u16 delta).  The staging area
 // takes the parents on the way in and the children on the way out, either
 //   rows           64 parents at stride kW|1 words, a parent's k children
 //                  side by side (+ separate output slices for the image), or
@@ -52,7 +54,8 @@ constexpr bool letter_blocks(bool inverse) {  // measured: W = 2 image and the p
 
 template <int W>
 static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
-  size_t per_warp = slice_stride<W>() * sizeof(u64);
+  // input slices (the image at W <= 6 keeps them in registers)
+  size_t per_warp = (inverse || W > 6) ? slice_stride<W>() * sizeof(u64) : 0;
   if (staged)
     per_warp += (letter_blocks<W>(inverse) ? static_cast<size_t>(k) * (64 * (W | 1) + 4)
                                            : static_cast<size_t>(64) * ((k * W) | 1)) *
@@ -70,10 +73,13 @@ static size_t sliced_smem(u32 k, u32 n, bool staged, bool inverse) {
 // rows sit at an ODD stride in words (W|1), so the lanes' row-strided 8-byte
 // accesses hit 16 distinct bank pairs (2 wavefronts, the minimum).
 // Unstaged (large k·W only): rows are read and written directly by lanes.
-// At least six 4-warp blocks per SM (<= 80 registers; image measured 0.86 ->
-// 0.81 ms at n=300 against the unconstrained allocation).
+// Register caps via minimum blocks per SM (4-warp blocks), measured on 2^24
+// parents: preimage 6 (<= 80 registers); image 6 at W <= 2, else 5 (<= 96:
+// the image holds its 2W input slices and 2W output slices in registers;
+// n=300 image 0.77 -> 0.75 ms at 5, n=100 0.32 -> 0.35 ms).
 template <int W, bool INV, bool STAGED>
-__global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
+__global__ void __launch_bounds__(kSliceWarps * 32, (INV || W <= 2) ? 6 : 5)
+    expand_sliced_kernel(
     const u64* __restrict__ src, u64 lo, u64 count, u32 n, u32 k,
     const uint16_t* __restrict__ g_img, u64* __restrict__ out, u32* __restrict__ out_card,
     u64* __restrict__ out_tag) {
@@ -90,8 +96,9 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
   const u32 kW = k * W;
   // e / kW == umulhi(e, magic) for the e < 64·kW used here (kW = 1: magic wraps to 0)
   const u32 magic = 0xFFFFFFFFu / kW + 1;
-  u64* sl = reinterpret_cast<u64*>(smem) + static_cast<size_t>(wid) * SS;
-  unsigned char* p = smem + static_cast<size_t>(kSliceWarps) * SS * sizeof(u64);
+  constexpr bool SL = INV || W > 6;  // input slices in shared memory
+  u64* sl = SL ? reinterpret_cast<u64*>(smem) + static_cast<size_t>(wid) * SS : nullptr;
+  unsigned char* p = smem + (SL ? static_cast<size_t>(kSliceWarps) * SS * sizeof(u64) : 0);
   u64* stage = nullptr;
   u32* scard = nullptr;
   u64* so = nullptr;
@@ -153,7 +160,11 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
       }
       __syncwarp();
     }
-    // ---- parents -> slices
+    // ---- parents -> slices: lane l ends up holding slices 64w + l and
+    // 64w + 32 + l — exactly the ones it scatters for the image, so the image
+    // keeps them in registers; the preimage gathers them from shared memory
+    constexpr bool REG = !INV && W <= 6;  // register budget: 2W slices + 2W outputs
+    u64 xs[REG ? W : 1][2];
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       u64 r0, r1;
@@ -166,8 +177,13 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
       }
       u64 c0, c1;
       transpose64(r0, r1, lane, c0, c1);
-      sl[64 * w + lane] = c0;
-      sl[64 * w + 32 + lane] = c1;
+      if constexpr (!REG) {
+        sl[64 * w + lane] = c0;
+        sl[64 * w + 32 + lane] = c1;
+      } else {
+        xs[w][0] = c0;
+        xs[w][1] = c1;
+      }
     }
     __syncwarp();
     for (u32 a = 0; a < k; ++a) {
@@ -180,11 +196,15 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 6) expand_sliced_kernel(
         for (int i = 0; i < 2 * W; ++i) o[32 * i + lane] = 0;
         __syncwarp();
         // two native 32-bit ORs (a 64-bit shared atomicOr is a CAS spin loop)
-        for (u32 q = lane; q < n; q += 32) {
-          const u64 v = sl[q];
-          u32* dst = reinterpret_cast<u32*>(&o[s_tab[base + q]]);
-          if (static_cast<u32>(v)) atomicOr(dst, static_cast<u32>(v));
-          if (v >> 32) atomicOr(dst + 1, static_cast<u32>(v >> 32));
+#pragma unroll
+        for (int j = 0; j < 2 * W; ++j) {
+          const u32 q = 32 * j + lane;
+          if (q < n) {
+            const u64 v = REG ? xs[REG ? j / 2 : 0][j % 2] : sl[q];
+            u32* dst = reinterpret_cast<u32*>(&o[s_tab[base + q]]);
+            if (static_cast<u32>(v)) atomicOr(dst, static_cast<u32>(v));
+            if (v >> 32) atomicOr(dst + 1, static_cast<u32>(v >> 32));
+          }
         }
         __syncwarp();
 #pragma unroll
