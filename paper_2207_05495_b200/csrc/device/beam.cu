@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kBeamThreads) beam_level_kernel(
 template <int W>
 __global__ void __launch_bounds__(kBeamThreads) beam_full_kernel(
     const uint16_t* __restrict__ g_img, u32 n, u32 k, u32 beam, u32 bc, u32 m2,
-    u32 max_levels, u64* __restrict__ level_tags, u32* __restrict__ result) {
+    u32 max_levels, u64* __restrict__ level_tags, u64* __restrict__ sav, u32* __restrict__ result) {
   extern __shared__ __align__(16) unsigned char smem[];
   const u32 mmax = bc * k;
   u64* cur = reinterpret_cast<u64*>(smem);                          // bc x W
@@ -117,16 +117,20 @@ __global__ void __launch_bounds__(kBeamThreads) beam_full_kernel(
   u32* idx = ncard + mmax;                                          // m2
   u32* keep = idx + m2;                                             // m2
   uint16_t* img = reinterpret_cast<uint16_t*>(keep + m2);           // k x n
-  __shared__ u32 s_kept, s_done;
+  __shared__ u32 s_kept, s_done, s_savn, s_same;
   for (u32 i = threadIdx.x; i < k * n; i += kBeamThreads) img[i] = g_img[i];
   for (u32 e = threadIdx.x; e < n * W; e += kBeamThreads) {  // level 0: the singletons
     const u32 q = e / W, w = e % W;
     cur[e] = (q >> 6) == w ? state_bit(q) : 0;
   }
   for (u32 q = threadIdx.x; q < n; q += kBeamThreads) ccard[q] = 1;
-  if (threadIdx.x == 0) s_done = 0;
+  if (threadIdx.x == 0) {
+    s_done = 0;
+    s_savn = 0xFFFFFFFFu;  // nothing saved yet
+  }
   __syncthreads();
   u32 ncur = n, level = 0;
+  bool cycle = false;
   while (level < max_levels) {
     ++level;
     const u32 m = ncur * k;
@@ -205,10 +209,30 @@ __global__ void __launch_bounds__(kBeamThreads) beam_full_kernel(
     __syncthreads();
     ncur = kept;
     if (s_done) break;
+    // A level's kept rows, in their canonical (card desc, lex) order, are a
+    // function of the previous level's alone: if they repeat, the search
+    // cycles and can never reach Q — the reference would run to its level
+    // cap and fail, so stop now (Brent: compare against the level saved at
+    // the last power of two).
+    if (threadIdx.x == 0) s_same = kept == s_savn ? 1u : 0u;
+    __syncthreads();
+    if (s_same)
+      for (u32 e = threadIdx.x; e < kept * W; e += kBeamThreads)
+        if (cur[e] != sav[e]) s_same = 0;
+    __syncthreads();
+    if (s_same) {
+      cycle = true;
+      break;
+    }
+    if ((level & (level - 1)) == 0) {
+      for (u32 e = threadIdx.x; e < kept * W; e += kBeamThreads) sav[e] = cur[e];
+      if (threadIdx.x == 0) s_savn = kept;
+    }
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
-    result[0] = s_done ? level : 0;  // level of the reset word (0: none)
-    result[1] = level;               // levels run
+    result[0] = s_done ? level : 0;         // level of the reset word (0: none)
+    result[1] = cycle ? 0xFFFFFFFFu : level;  // levels run (all ones: a cycle)
   }
 }
 
@@ -223,15 +247,19 @@ BeamRun beam_full_small(Context& c, size_t beam, u64 level_cap, std::vector<u32>
   const size_t smem = bc * W * 8 + mmax * W * 8 + bc * 4 + mmax * 4 + m2 * 8 +
                       ((static_cast<size_t>(k) * n * 2 + 15) & ~size_t{15});
   if (mmax > 8192 || smem > kBeamSmem) return BeamRun::NotApplicable;
-  const u64 max_levels = std::min<u64>(level_cap, 4096);
+  // the whole search in one launch while its tags fit 64 MB (a cycling beam
+  // stops at the repeat; beam_ibfs's host loop only takes what is left over)
+  const u64 max_levels =
+      std::min<u64>(level_cap, std::max<u64>(4096, (u64{64} << 20) / (beam * 8)));
   cudaStream_t s = as_stream(c.stream());
   u64* tags = static_cast<u64*>(c.alloc(max_levels * beam * 8));
+  u64* sav = static_cast<u64*>(c.alloc(bc * W * 8));
   u32* res = static_cast<u32*>(c.scratch(7, 64));
   SW_DISPATCH_W(c.W(), {
     smem_opt_in(reinterpret_cast<const void*>(beam_full_kernel<W>), static_cast<int>(kBeamSmem));
     beam_full_kernel<W><<<1, kBeamThreads, smem, s>>>(
         static_cast<const uint16_t*>(c.d_img), n, k, static_cast<u32>(beam), static_cast<u32>(bc),
-        static_cast<u32>(m2), static_cast<u32>(max_levels), tags, res);
+        static_cast<u32>(m2), static_cast<u32>(max_levels), tags, sav, res);
   });
   SW_CHECK_LAUNCH();
   c.counters.kernel_launches += 1;
@@ -253,6 +281,7 @@ BeamRun beam_full_small(Context& c, size_t beam, u64 level_cap, std::vector<u32>
     out = h[1] >= level_cap ? BeamRun::NotFound : BeamRun::NotApplicable;  // out of level room
   }
   c.free(tags);
+  c.free(sav);
   return out;
 }
 
