@@ -11,7 +11,8 @@ measured in ONE run on the GPU box (its own host cores for the reference):
 Writes one JSON object (stdout and the path given).  The reference is
 oracle/_ref (the unmodified headers, -O3), test infrastructure only.
 Usage: python scripts/baselines.py OUT.json [--skip-full]"""
-import json, os, sys, tempfile, time
+import json
+import subprocess, os, sys, tempfile, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2207_05495_b200 import native as sw  # noqa: E402
@@ -76,6 +77,14 @@ with tempfile.TemporaryDirectory() as td:
         t = time.perf_counter()
         sw.run_experiment([100], 2, 1000, 0, p, solver="exact", threads=threads, deterministic=True)
         rows[f"gpu_threads{threads}_s"] = time.perf_counter() - t
+    # the same batch in a FRESH process (CUDA context creation, module loading and
+    # the interpreter start included) — what a one-off batch run costs
+    child = ("import sys; sys.path.insert(0, {r!r}); from paper_2207_05495_b200 import native as sw; "
+             "sw.run_experiment([100], 2, 1000, 0, {p!r}, solver='exact', threads=16, "
+             "deterministic=True)").format(r=ROOT, p=os.path.join(td, "cold.csv"))
+    t = time.perf_counter()
+    subprocess.run([sys.executable, "-c", child], check=True)
+    rows["gpu_cold_process_threads16_s"] = time.perf_counter() - t
     ok = 0
     for line in open(p).read().splitlines()[1:]:
         f = line.split(",")
@@ -91,6 +100,9 @@ rows["gpu_matches_golden"] = ok
 best = min(v for k, v in rows.items() if k.startswith("gpu_threads"))
 rows["gpu_instances_per_s"] = 1000 / best
 rows["ref_instances_per_s"] = 1000 / rows["ref_all_cores_s"]
+rows["gpu_cold_process_instances_per_s"] = 1000 / rows["gpu_cold_process_threads16_s"]
+rows["note"] = ("gpu_threads*: warm process (context and kernels loaded by the solves above); "
+                "gpu_cold_process*: a fresh interpreter + CUDA context for the batch alone")
 out["batch_n100"] = rows
 print(json.dumps({"batch_n100": rows}), flush=True)
 json.dump(out, open(sys.argv[1], "w"), indent=1)
