@@ -152,8 +152,17 @@ __global__ void map_flags_kernel(const uint8_t* __restrict__ src, const u32* __r
 
 // Warp work pool over (query, node) tasks.  MARK: keep[j] = 0 for queries with
 // a (proper) subset among the keys; EXIST: *found / wit on the first hit.
+#ifndef SW_TRIE_SLOTS_WIDE
+#define SW_TRIE_SLOTS_WIDE 4
+#endif
+template <int W>
+constexpr int kTrieSlots = W <= 6 ? 2 : SW_TRIE_SLOTS_WIDE;
+#ifndef SW_TRIE_MINB_NARROW
+#define SW_TRIE_MINB_NARROW 4
+#endif
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) trie_pool_kernel(
+__global__ void __launch_bounds__(kThreads, (W <= 6 ? SW_TRIE_MINB_NARROW : (W <= 10 ? 3 : 1)))
+    trie_pool_kernel(
     const u64* __restrict__ K, const ulonglong2* __restrict__ Ksig,
     const TrieNode* __restrict__ nodes, const ulonglong2* __restrict__ psig,
     const u64* __restrict__ Q, const ulonglong2* __restrict__ Qsig, u32 Nq, uint8_t* keep,
@@ -161,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
     unsigned long long* wit, u32* next_query, uint4* spill_all, u32* overflow_scans,
     unsigned long long* stats, u32 root_div, u32 spill_cap) {
   constexpr int P = Pad<W>::P;
+  constexpr int S = kTrieSlots<W>;
   __shared__ u32 s_q[kWarps][kCap];
   __shared__ u32 s_n[kWarps][kCap];
   __shared__ u32 s_c[kWarps][kCap];
@@ -193,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
       if (found_seen) break;
       found_seen = *reinterpret_cast<volatile int*>(found);
     }
-    if (sp < 32 && gsp > 0) {
+    if (sp < 32 * S && gsp > 0) {
       const int t = gsp < kSpillHalf ? gsp : kSpillHalf;
       for (int i = lane; i < t; i += 32) {
         const uint4 v = spill[gsp - t + i];
@@ -204,12 +214,13 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
       gsp -= t;
       sp += t;
       __syncwarp();
-    } else if (sp < 32 && more) {
+    } else if (sp < 32 * S && more) {  // up to 32 new queries per refill
+      const u32 want = static_cast<u32>(32 * S - sp < 32 ? 32 * S - sp : 32);
       u32 base = 0;
-      if (lane == 0) base = atomicAdd(next_query, static_cast<u32>(32 - sp));
+      if (lane == 0) base = atomicAdd(next_query, want);
       base = __shfl_sync(FULL, base, 0);
-      const u32 got = base >= Nq ? 0 : min(static_cast<u32>(32 - sp), Nq - base);
-      if (base + (32 - sp) >= Nq) more = false;
+      const u32 got = base >= Nq ? 0 : min(want, Nq - base);
+      if (base + want >= Nq) more = false;
       const u32 j = base + lane;
       bool push = static_cast<u32>(lane) < got;
       const u32 cy = push ? static_cast<u32>(Q[static_cast<u64>(j) * P + W]) : 0;
@@ -228,148 +239,170 @@ __global__ void __launch_bounds__(kThreads, (W <= 6 ? 6 : (W <= 10 ? 3 : 1))) tr
       if (!more && gsp == 0) break;
       continue;
     }
-    const int take = sp < 32 ? sp : 32;
-    bool have = lane < take;
-    u32 j = 0, id = 0, cy = 0, dv = 0xFFFF;
-    if (have) {
-      const int pos = sp - 1 - lane;
-      j = sq[pos];
-      id = sn[pos];
-      cy = sc[pos] & 0xFFFF;
-      dv = sc[pos] >> 16;  // the node's division state, carried by the task
+    // S tasks per lane per round (slots): all slots' node, filter and
+    // query-word loads are issued together, so each lane keeps S L2 round
+    // trips in flight (the walk is latency-bound: ncu at n=300 showed 0.31
+    // issued warps per scheduler with one task per lane; n=570, first 45 DFS
+    // launches: 6.38 s with one slot, 5.02 s with two, 4.62 s with three, 4.44 s
+    // with four — the W > 6 default; n=300 (two slots) is insensitive).
+    const int take = sp < 32 * S ? sp : 32 * S;
+    bool have[S];
+    u32 j[S], id[S], cy[S], dv[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      have[s] = lane + 32 * s < take;
+      j[s] = 0;
+      id[s] = 0;
+      cy[s] = 0;
+      dv[s] = 0xFFFF;
+      if (have[s]) {
+        const int pos = sp - 1 - lane - 32 * s;
+        j[s] = sq[pos];
+        id[s] = sn[pos];
+        cy[s] = sc[pos] & 0xFFFF;
+        dv[s] = sc[pos] >> 16;  // the node's division state, carried by the task
+      }
     }
     sp -= take;
     __syncwarp();
-    if (!EXIST && have && shit[j % kHitSlots] == j) have = false;
-    const u32 limit = PROPER ? cy - 1 : cy;
-
-    // ---- one round of independent loads: the node, the query's filter words
-    // and the query word holding the node's division state (carried by the task)
-    TrieNode nd{};
-    ulonglong2 qs = make_ulonglong2(0, 0), zsig = make_ulonglong2(0, 0),
-               osig = make_ulonglong2(0, 0);
-    u64 yw = 0;
-    if (have) {
-      nd = load_trie_node(nodes + id);
-      qs = __ldg(Qsig + j);
-      if (dv != 0xFFFF) yw = __ldg(Q + static_cast<u64>(j) * P + (dv >> 6));
-      if (kPayloadSig) {
-        zsig = __ldg(psig + 2 * static_cast<u64>(id));
-        osig = __ldg(psig + 2 * static_cast<u64>(id) + 1);
+    // ---- one round of independent loads: the nodes, the queries' filter words
+    // and the query words holding the nodes' division states
+    TrieNode nd[S];
+    ulonglong2 qs[S], zsig[S], osig[S];
+    u64 yw[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (!EXIST && have[s] && shit[j[s] % kHitSlots] == j[s]) have[s] = false;
+      nd[s] = TrieNode{};
+      qs[s] = zsig[s] = osig[s] = make_ulonglong2(0, 0);
+      yw[s] = 0;
+      if (have[s]) {
+        nd[s] = load_trie_node(nodes + id[s]);
+        qs[s] = __ldg(Qsig + j[s]);
+        if (dv[s] != 0xFFFF) yw[s] = __ldg(Q + static_cast<u64>(j[s]) * P + (dv[s] >> 6));
+        if (kPayloadSig) {
+          zsig[s] = __ldg(psig + 2 * static_cast<u64>(id[s]));
+          osig[s] = __ldg(psig + 2 * static_cast<u64>(id[s]) + 1);
+        }
       }
     }
-    // ---- evaluate: zero side always, one side iff y holds the division state
-    u32 c0 = kNo, c1 = kNo, zlo = 0, zn = 0, olo = 0, on = 0;
-    if (have && nd.minc <= limit) {
-      if (nd.zero != kNo) {
-        c0 = nd.zero;
-      } else if (!kPayloadSig || sig_pass(zsig, qs)) {
-        zlo = nd.lo;
-        zn = nd.mid - nd.lo;
-      }
-      if (dv != 0xFFFF) {
-        if ((yw >> (63 - (dv & 63))) & 1) {
-          if (nd.one != kNo) {
-            c1 = nd.one;
-          } else if (!kPayloadSig || sig_pass(osig, qs)) {
-            olo = nd.mid;
-            on = nd.hi - nd.mid;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const u32 limit = PROPER ? cy[s] - 1 : cy[s];
+      // ---- evaluate: zero side always, one side iff y holds the division state
+      u32 c0 = kNo, c1 = kNo, zlo = 0, zn = 0, olo = 0, on = 0;
+      if (have[s] && nd[s].minc <= limit) {
+        if (nd[s].zero != kNo) {
+          c0 = nd[s].zero;
+        } else if (!kPayloadSig || sig_pass(zsig[s], qs[s])) {
+          zlo = nd[s].lo;
+          zn = nd[s].mid - nd[s].lo;
+        }
+        if (dv[s] != 0xFFFF) {
+          if ((yw[s] >> (63 - (dv[s] & 63))) & 1) {
+            if (nd[s].one != kNo) {
+              c1 = nd[s].one;
+            } else if (!kPayloadSig || sig_pass(osig[s], qs[s])) {
+              olo = nd[s].mid;
+              on = nd[s].hi - nd[s].mid;
+            }
           }
         }
       }
-    }
-    if (stats) {
-      const u32 v[3] = {static_cast<u32>(__popc(__ballot_sync(FULL, have))),
-                        static_cast<u32>(__popc(__ballot_sync(FULL, c0 != kNo))),
-                        static_cast<u32>(__popc(__ballot_sync(FULL, c1 != kNo)))};
-      if (lane == 0) {
+      if (stats) {
+        const u32 v[3] = {static_cast<u32>(__popc(__ballot_sync(FULL, have[s]))),
+                          static_cast<u32>(__popc(__ballot_sync(FULL, c0 != kNo))),
+                          static_cast<u32>(__popc(__ballot_sync(FULL, c1 != kNo)))};
+        if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) atomicAdd(stats + q, static_cast<unsigned long long>(v[q]));
-      }
-    }
-    // ---- push children
-    const unsigned m0 = __ballot_sync(FULL, c0 != kNo);
-    const unsigned m1 = __ballot_sync(FULL, c1 != kNo);
-    const int n0 = __popc(m0), n1 = __popc(m1);
-    if (sp + n0 + n1 > kCap && gsp + kSpillHalf <= static_cast<int>(spill_cap)) {
-      for (int i = lane; i < kSpillHalf; i += 32) spill[gsp + i] = make_uint4(sq[i], sn[i], sc[i], 0);
-      __syncwarp();
-      for (int i = lane; i < sp - kSpillHalf; i += 32) {
-        sq[i] = sq[i + kSpillHalf];
-        sn[i] = sn[i + kSpillHalf];
-        sc[i] = sc[i + kSpillHalf];
-      }
-      __syncwarp();
-      gsp += kSpillHalf;
-      sp -= kSpillHalf;
-    }
-    if (sp + n0 + n1 > kCap) {  // pool and spill stack full: scan the children's ranges
-      if (c0 != kNo) {
-        zlo = nd.lo;
-        zn = nd.mid - nd.lo;
-      }
-      if (c1 != kNo) {
-        olo = nd.mid;
-        on = nd.hi - nd.mid;
-      }
-      if (lane == 0) atomicAdd(overflow_scans, 1u);
-    } else {
-      if (c1 != kNo) {
-        const int pos = sp + __popc(m1 & lt);
-        sq[pos] = j;
-        sn[pos] = c1;
-        sc[pos] = cy | (nd.child_div & 0xFFFF0000u);
-      }
-      if (c0 != kNo) {
-        const int pos = sp + n1 + __popc(m0 & lt);
-        sq[pos] = j;
-        sn[pos] = c0;
-        sc[pos] = cy | (nd.child_div << 16);
-      }
-      sp += n0 + n1;
-    }
-    __syncwarp();
-
-    // ---- payload scan: (key, query) pairs of the round flattened over lanes
-    const u32 cnt = zn + on;
-    u32 incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 v = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const u32 total = __shfl_sync(FULL, incl, 31);
-    if (stats && lane == 0) atomicAdd(stats + 3, static_cast<unsigned long long>(total));
-    const u32 excl = incl - cnt;
-    for (u32 base = 0; base < total; base += 32) {
-      const u32 t = base + lane;
-      int owner = 0;
-#pragma unroll
-      for (int s = 16; s; s >>= 1) {
-        const u32 v = __shfl_sync(FULL, incl, owner + s - 1);
-        if (v <= t) owner += s;
-      }
-      owner = owner > 31 ? 31 : owner;
-      const u32 o_excl = __shfl_sync(FULL, excl, owner);
-      const u32 o_zlo = __shfl_sync(FULL, zlo, owner);
-      const u32 o_zn = __shfl_sync(FULL, zn, owner);
-      const u32 o_olo = __shfl_sync(FULL, olo, owner);
-      const u32 o_j = __shfl_sync(FULL, j, owner);
-      const u32 o_lim = __shfl_sync(FULL, limit, owner);
-      const ulonglong2 oq = make_ulonglong2(__shfl_sync(FULL, qs.x, owner),
-                                            __shfl_sync(FULL, qs.y, owner));
-      if (t < total) {
-        const u32 r = t - o_excl;
-        const u32 key = r < o_zn ? o_zlo + r : o_olo + (r - o_zn);
-        if (sig_pass(__ldg(Ksig + key), oq)) {  // rare: the exact test
-          const u64* kr = K + static_cast<u64>(key) * P;
-          const u64* yr = Q + static_cast<u64>(o_j) * P;
-          u64 acc = 0;
-#pragma unroll
-          for (int w = 0; w < W; ++w) acc |= __ldg(kr + w) & ~__ldg(yr + w);
-          if (static_cast<u32>(__ldg(kr + W)) <= o_lim && acc == 0) report(key, o_j);
+          for (int q = 0; q < 3; ++q) atomicAdd(stats + q, static_cast<unsigned long long>(v[q]));
         }
       }
+      // ---- push children
+      const unsigned m0 = __ballot_sync(FULL, c0 != kNo);
+      const unsigned m1 = __ballot_sync(FULL, c1 != kNo);
+      const int n0 = __popc(m0), n1 = __popc(m1);
+      if (sp + n0 + n1 > kCap && gsp + kSpillHalf <= static_cast<int>(spill_cap)) {
+        for (int i = lane; i < kSpillHalf; i += 32) spill[gsp + i] = make_uint4(sq[i], sn[i], sc[i], 0);
+        __syncwarp();
+        for (int i = lane; i < sp - kSpillHalf; i += 32) {
+          sq[i] = sq[i + kSpillHalf];
+          sn[i] = sn[i + kSpillHalf];
+          sc[i] = sc[i + kSpillHalf];
+        }
+        __syncwarp();
+        gsp += kSpillHalf;
+        sp -= kSpillHalf;
+      }
+      if (sp + n0 + n1 > kCap) {  // pool and spill stack full: scan the children's ranges
+        if (c0 != kNo) {
+          zlo = nd[s].lo;
+          zn = nd[s].mid - nd[s].lo;
+        }
+        if (c1 != kNo) {
+          olo = nd[s].mid;
+          on = nd[s].hi - nd[s].mid;
+        }
+        if (lane == 0) atomicAdd(overflow_scans, 1u);
+      } else {
+        if (c1 != kNo) {
+          const int pos = sp + __popc(m1 & lt);
+          sq[pos] = j[s];
+          sn[pos] = c1;
+          sc[pos] = cy[s] | (nd[s].child_div & 0xFFFF0000u);
+        }
+        if (c0 != kNo) {
+          const int pos = sp + n1 + __popc(m0 & lt);
+          sq[pos] = j[s];
+          sn[pos] = c0;
+          sc[pos] = cy[s] | (nd[s].child_div << 16);
+        }
+        sp += n0 + n1;
+      }
+      __syncwarp();
+
+      // ---- payload scan: (key, query) pairs of this slot flattened over lanes
+      const u32 cnt = zn + on;
+      u32 incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const u32 total = __shfl_sync(FULL, incl, 31);
+      if (stats && lane == 0) atomicAdd(stats + 3, static_cast<unsigned long long>(total));
+      const u32 excl = incl - cnt;
+      for (u32 base = 0; base < total; base += 32) {
+        const u32 t = base + lane;
+        int owner = 0;
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) {
+          const u32 v = __shfl_sync(FULL, incl, owner + sh - 1);
+          if (v <= t) owner += sh;
+        }
+        owner = owner > 31 ? 31 : owner;
+        const u32 o_excl = __shfl_sync(FULL, excl, owner);
+        const u32 o_zlo = __shfl_sync(FULL, zlo, owner);
+        const u32 o_zn = __shfl_sync(FULL, zn, owner);
+        const u32 o_olo = __shfl_sync(FULL, olo, owner);
+        const u32 o_j = __shfl_sync(FULL, j[s], owner);
+        const u32 o_lim = __shfl_sync(FULL, limit, owner);
+        const ulonglong2 oq = make_ulonglong2(__shfl_sync(FULL, qs[s].x, owner),
+                                              __shfl_sync(FULL, qs[s].y, owner));
+        if (t < total) {
+          const u32 r = t - o_excl;
+          const u32 key = r < o_zn ? o_zlo + r : o_olo + (r - o_zn);
+          if (sig_pass(__ldg(Ksig + key), oq)) {  // rare: the exact test
+            const u64* kr = K + static_cast<u64>(key) * P;
+            const u64* yr = Q + static_cast<u64>(o_j) * P;
+            u64 acc = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc |= __ldg(kr + w) & ~__ldg(yr + w);
+            if (static_cast<u32>(__ldg(kr + W)) <= o_lim && acc == 0) report(key, o_j);
+          }
+        }
+      }
+      __syncwarp();
     }
     __syncwarp();
   }

@@ -323,7 +323,8 @@ def test_containment_pool_overflow_scan_path(gpu, ref, spill_cap, index):
     assert scans and max(scans) > 0, "overflow path not exercised"
 
 
-@pytest.mark.parametrize("n,da,db,seed", [(100, 0.1, 0.4, 0), (300, 0.08, 0.3, 1), (64, 0.3, 0.3, 3)])
+@pytest.mark.parametrize("n,da,db,seed", [(100, 0.1, 0.4, 0), (300, 0.08, 0.3, 1), (64, 0.3, 0.3, 3),
+                                         (570, 0.05, 0.2, 2), (1000, 0.03, 0.15, 4)])
 def test_trie_exists_any_key_order(gpu, ref, n, da, db, seed):
     """The trie index (device/trie_query.cu) over keys in ANY order (the engine
     indexes L_BFS in hash order): one planted containment is found wherever it
