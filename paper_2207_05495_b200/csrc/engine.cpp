@@ -151,6 +151,34 @@ std::vector<u64> GpuBibfs::level_tags(const DList& l) {
   return dev::read_tags(ctx_, gather(l, true));
 }
 
+GpuBibfs::LevelTags GpuBibfs::level_tags_of(const DList& l) {
+  LevelTags t;
+  if (dist() || !l.tagged()) {
+    t.host = level_tags(l);
+    return t;
+  }
+  t.ctx = &ctx_;
+  t.dev = static_cast<u64*>(ctx_.alloc(std::max<size_t>(l.size(), 1) * 8));
+  ctx_.memcpy_d2d(t.dev, l.tags, l.size() * 8);
+  return t;
+}
+
+GpuBibfs::LevelTags::~LevelTags() {
+  if (ctx && dev) {
+    try {
+      ctx->free(dev);
+    } catch (...) {
+    }
+  }
+}
+
+u64 GpuBibfs::LevelTags::at(size_t i) const {
+  if (!dev) return host[i];
+  u64 t = 0;
+  ctx->memcpy_d2h(&t, dev + i, 8);
+  return t;
+}
+
 // set_list.hpp:171-174
 double GpuBibfs::density(const Info& i) const {
   if (i.size == 0 || n_ == 0) return 0.0;
@@ -359,7 +387,7 @@ void GpuBibfs::bfs_step(bool with_history) {
   refresh_part(*lbfs_, lbfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
-  if (opt_.track_word) bfs_levels_.push_back(level_tags(*lbfs_));
+  if (opt_.track_word) bfs_levels_.push_back(level_tags_of(*lbfs_));
   ratio_bfs_[0] = 0.5 * ratio_bfs_[0] + 0.5 * r_dupl;
   ratio_bfs_[1] = 0.5 * ratio_bfs_[1] + 0.5 * r_self;
   if (with_history) ratio_bfs_[2] = 0.5 * ratio_bfs_[2] + 0.5 * r_hist;
@@ -431,7 +459,7 @@ void GpuBibfs::ibfs_step(bool with_history) {
   refresh_part(*libfs_, libfs_i_);
   charged_layer_ = 0;
   rb.armed = false;
-  if (opt_.track_word) ibfs_levels_.push_back(level_tags(*libfs_));
+  if (opt_.track_word) ibfs_levels_.push_back(level_tags_of(*libfs_));
   ratio_ibfs_[0] = 0.5 * ratio_ibfs_[0] + 0.5 * r_dupl;
   ratio_ibfs_[1] = 0.5 * ratio_ibfs_[1] + 0.5 * r_self;
   if (with_history) ratio_ibfs_[2] = 0.5 * ratio_ibfs_[2] + 0.5 * r_hist;
@@ -873,7 +901,7 @@ Word GpuBibfs::bfs_prefix(size_t index) const {
   Word w;
   size_t idx = index;
   for (size_t lvl = bfs_levels_.size(); lvl-- > 0;) {
-    const u64 tag = bfs_levels_[lvl][idx];
+    const u64 tag = bfs_levels_[lvl].at(idx);
     w.push_back(static_cast<u32>(tag & 0xFFFF));
     idx = static_cast<size_t>(tag >> 16);
   }
@@ -886,14 +914,14 @@ Word GpuBibfs::ibfs_suffix_from_tag(u64 tag) const {
   for (size_t lvl = ibfs_levels_.size(); lvl-- > 0;) {
     w.push_back(static_cast<u32>(tag & 0xFFFF));
     if (lvl == 0) break;
-    tag = ibfs_levels_[lvl - 1][static_cast<size_t>(tag >> 16)];
+    tag = ibfs_levels_[lvl - 1].at(static_cast<size_t>(tag >> 16));
   }
   return w;
 }
 
 Word GpuBibfs::ibfs_suffix_from_index(size_t index) const {
   if (ibfs_levels_.empty()) return {};
-  return ibfs_suffix_from_tag(ibfs_levels_.back()[index]);
+  return ibfs_suffix_from_tag(ibfs_levels_.back().at(index));
 }
 
 // bibfs_engine.hpp:442-460 (same keys, same default ostream formatting).

@@ -185,7 +185,23 @@ class GpuBibfs {
   std::array<double, 3> ratio_bfs_{0, 0, 0}, ratio_ibfs_{0, 0, 0};
   std::array<bool, 4> failed_{false, false, false, false};
   u64 charged_layer_ = 0;
-  std::vector<std::vector<u64>> bfs_levels_, ibfs_levels_;
+  // Parent records (tags) of every BFS / IBFS level for word reconstruction
+  // (bibfs_engine.hpp:301-328): kept on the device and read one entry per level
+  // while walking back (a solve used to download every level's tags — 30 MB
+  // per n=300 solve); the partitioned solve gathers them on the host.
+  struct LevelTags {
+    dev::Context* ctx = nullptr;
+    u64* dev = nullptr;
+    std::vector<u64> host;
+    LevelTags() = default;
+    LevelTags(const LevelTags&) = delete;
+    LevelTags& operator=(const LevelTags&) = delete;
+    LevelTags(LevelTags&& o) noexcept : ctx(o.ctx), dev(o.dev), host(std::move(o.host)) { o.dev = nullptr; }
+    ~LevelTags();
+    u64 at(size_t i) const;
+  };
+  LevelTags level_tags_of(const dev::DList& l);
+  std::vector<LevelTags> bfs_levels_, ibfs_levels_;
   // L_BFS lists met (meet_check, no tracking) since L_IBFS was last committed,
   // oldest first; lbfs_met_: the current L_BFS has been met too.
   std::vector<std::unique_ptr<dev::DList>> met_lists_;
