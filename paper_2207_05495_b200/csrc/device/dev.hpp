@@ -194,6 +194,7 @@ ListStats stats(Context& c, const DList& l);
 // ---- ordering and deduplication (set_list.hpp:210-265)
 void sort_lex(Context& c, DList& l);                   // stable, index tie-break
 void sort_card_desc_lex(Context& c, DList& l);         // card desc, lex, index
+void sort_card_desc(Context& c, DList& l);             // card desc, stable (no lex order)
 size_t dedupe_sorted(Context& c, DList& l);            // returns #removed
 size_t lex_sort_dedupe(Context& c, DList& l);          // returns #removed
 // Set-semantics dedupe by open-addressing hash (dedupe.cu): one row per

@@ -158,6 +158,31 @@ void sort_card_desc_lex(Context& c, DList& l) {
   compact_flags(c, l, nullptr, perm);
 }
 
+// Cardinality classes only (descending, stable): a radix sort of the card key
+// alone (<= 11 bits) instead of the full (card, lex) key — the relaxed DFS
+// slice order needs the classes together, not lex order inside them.
+void sort_card_desc(Context& c, DList& l) {
+  const u64 N = l.size();
+  if (N <= 1) return;
+  cudaStream_t s = as_stream(c.stream());
+  u32* p0 = static_cast<u32*>(c.scratch(2, N * 4));
+  u32* p1 = static_cast<u32*>(c.scratch(3, N * 4));
+  iota_kernel<<<grid_for(N, 256), 256, 0, s>>>(p0, N);
+  u32* k0 = static_cast<u32*>(c.scratch(0, N * 8));
+  u32* k1 = static_cast<u32*>(c.scratch(1, N * 8));
+  cub::DoubleBuffer<u32> vals(p0, p1), ck(k0, k1);
+  card_key_kernel<<<grid_for(N, 256), 256, 0, s>>>(l.cards, vals.Current(), N, c.n(), ck.Current());
+  int bits = 1;
+  while ((1u << bits) <= c.n()) ++bits;
+  size_t tb = 0;
+  SW_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck, vals, static_cast<int>(N), 0, bits, s));
+  void* t = c.scratch(4, tb);
+  SW_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, ck, vals, static_cast<int>(N), 0, bits, s));
+  SW_CHECK_LAUNCH();
+  c.counters.kernel_launches += 2 + (bits + 7) / 8;
+  compact_flags(c, l, nullptr, vals.Current());
+}
+
 size_t dedupe_sorted(Context& c, DList& l) {
   if (l.size() <= 1) return 0;
   const size_t before = l.size();
