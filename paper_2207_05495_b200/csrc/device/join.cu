@@ -127,23 +127,48 @@ struct JoinBlock {
   u32 c_lo, c_hi;  // candidate range of its bucket
 };
 
+// Projection of a row on up to 64 states (bit i = the row holds pstate[i]):
+// y ⊆ x implies proj(y) ⊆ proj(x), so a one-word test rejects most candidate
+// pairs before the W-word comparison.  The states are the ones rarest in X
+// (a query holding one of them fits few candidates).
+template <int W>
+__global__ void project_kernel(const u64* __restrict__ rows, u64 count,
+                               const uint16_t* __restrict__ pstate, u32 np, u64* __restrict__ proj) {
+  __shared__ uint16_t sp[64];
+  if (threadIdx.x < np) sp[threadIdx.x] = pstate[threadIdx.x];
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64* r = rows + i * W;
+    u64 p = 0;
+    for (u32 b = 0; b < np; ++b) {
+      const u32 q = sp[b];
+      p |= ((r[q >> 6] >> (63 - (q & 63))) & 1ull) << b;
+    }
+    proj[i] = p;
+  }
+}
+
 template <int W, bool PROPER>
 __global__ void __launch_bounds__(kJoinThreads) superset_join_kernel(
     const u64* __restrict__ X, const u32* __restrict__ Xcard, const u64* __restrict__ Y,
     const u32* __restrict__ Ycard, const u32* __restrict__ qidx, const u32* __restrict__ cval,
-    const JoinBlock* __restrict__ blocks, uint8_t* __restrict__ keep) {
+    const JoinBlock* __restrict__ blocks, const u64* __restrict__ Xproj,
+    const u64* __restrict__ Yproj, uint8_t* __restrict__ keep) {
   __shared__ u64 s_rows[kJoinTile][W];
   __shared__ u32 s_card[kJoinTile];
+  __shared__ u64 s_proj[kJoinTile];
   const JoinBlock jb = blocks[blockIdx.x];
   const u32 t = threadIdx.x;
   const bool have = jb.q_lo + t < jb.q_hi;
   u32 j = 0, cy = 0;
-  u64 y[W];
+  u64 y[W], py = 0;
 #pragma unroll
   for (int w = 0; w < W; ++w) y[w] = 0;
   if (have) {
     j = qidx[jb.q_lo + t];
     cy = Ycard[j];
+    py = Yproj[j];
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = Y[static_cast<u64>(j) * W + w];
   }
@@ -154,6 +179,7 @@ __global__ void __launch_bounds__(kJoinThreads) superset_join_kernel(
     for (u32 r = t; r < cnt; r += kJoinThreads) {
       const u32 x = cval[base + r];
       s_card[r] = Xcard[x];
+      s_proj[r] = Xproj[x];
 #pragma unroll
       for (int w = 0; w < W; ++w) s_rows[r][w] = X[static_cast<u64>(x) * W + w];
     }
@@ -165,6 +191,7 @@ __global__ void __launch_bounds__(kJoinThreads) superset_join_kernel(
           active = false;
           break;
         }
+        if (py & ~s_proj[r]) continue;  // a projected state of y is missing from x
         u64 bad = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w) bad |= y[w] & ~s_rows[r][w];
@@ -223,6 +250,21 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
                    [&](uint16_t a, uint16_t b) { return hhist[a] < hhist[b]; });
   uint16_t* dorder = static_cast<uint16_t*>(c.alloc(n * 2));
   c.memcpy_h2d(dorder, order.data(), n * 2);
+  // projection states: the (up to) 64 rarest states that some x holds
+  std::vector<uint16_t> pst;
+  for (u32 i = 0; i < n && pst.size() < 64; ++i)
+    if (hhist[order[i]] > 0) pst.push_back(order[i]);
+  uint16_t* dpst = static_cast<uint16_t*>(c.alloc(64 * 2));
+  if (!pst.empty()) c.memcpy_h2d(dpst, pst.data(), pst.size() * 2);
+  u64* xproj = static_cast<u64*>(c.alloc(nx * 8));
+  u64* yproj = static_cast<u64*>(c.alloc(ny * 8));
+  SW_DISPATCH_W(c.W(), {
+    project_kernel<W><<<grid_for(nx, 256), 256, 0, s>>>(X.words, nx, dpst,
+                                                        static_cast<u32>(pst.size()), xproj);
+    project_kernel<W><<<grid_for(ny, 256), 256, 0, s>>>(Y.words, ny, dpst,
+                                                        static_cast<u32>(pst.size()), yproj);
+  });
+  SW_CHECK_LAUNCH();
   // 2. rarest state of every query; sort queries by (r, |y|)
   u32* qkey = static_cast<u32*>(c.alloc(ny * 4));
   u32* qkey2 = static_cast<u32*>(c.alloc(ny * 4));
@@ -325,10 +367,10 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
     SW_DISPATCH_W(c.W(), {
       if (proper)
         superset_join_kernel<W, true><<<static_cast<unsigned>(blocks.size()), kJoinThreads, 0, s>>>(
-            X.words, X.cards, Y.words, Y.cards, qidx, cval, dblocks, keep);
+            X.words, X.cards, Y.words, Y.cards, qidx, cval, dblocks, xproj, yproj, keep);
       else
         superset_join_kernel<W, false><<<static_cast<unsigned>(blocks.size()), kJoinThreads, 0, s>>>(
-            X.words, X.cards, Y.words, Y.cards, qidx, cval, dblocks, keep);
+            X.words, X.cards, Y.words, Y.cards, qidx, cval, dblocks, xproj, yproj, keep);
     });
     SW_CHECK_LAUNCH();
     c.free(dblocks);
@@ -340,7 +382,10 @@ void superset_keep_flags(Context& c, const DList& X, const DList& Y, bool proper
     empty_query_kernel<<<grid_for(ny, 256), 256, 0, s>>>(Y.cards, ny, keep, any_fit);
     SW_CHECK_LAUNCH();
   }
-  c.counters.kernel_launches += 8;
+  c.counters.kernel_launches += 10;
+  c.free(dpst);
+  c.free(xproj);
+  c.free(yproj);
   c.free(hist);
   c.free(dorder);
   c.free(qkey);
