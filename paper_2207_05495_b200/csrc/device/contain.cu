@@ -959,6 +959,8 @@ size_t self_reduce_minimal(Context& c, DList& l) {
     return before - compact_flags(c, l, keep, nullptr);
   }
   if (use_trie_for_marks()) return trie_self_reduce_minimal(c, l);
+  // Rarest states first (measured at n=300 s0: engine 98 ms; most frequent first
+  // 187 ms, natural order 119 ms).
   const PermIndex p = build_perm_index(c, l, StateOrder::FreqAsc);
   // The queries are the keys themselves: query with the index's own sorted,
   // relabelled rows (best locality), then map the flags back to l's order.
