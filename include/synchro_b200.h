@@ -127,6 +127,14 @@ uint64_t sw_instance_seed(uint64_t seed_base, uint32_t n, uint32_t index);
 int sw_parse_automaton(const char* text, uint32_t* n, uint32_t* k, uint32_t* delta_out,
                        size_t delta_cap);
 int sw_is_synchronizing(uint32_t n, uint32_t k, const uint32_t* delta, int32_t* result);
+
+/* Shortest merging word length of every state pair {p <= q}, at q(q+1)/2 + p
+ * (UINT32_MAX: unmergeable) — the pair automaton BFS behind is_synchronizing
+ * (automaton.hpp:119-157) and Eppstein's bound (heuristics.hpp:26-79).
+ * on_device != 0: the GPU BFS (device/pairs.cu); 0: the host BFS.  `cap` >=
+ * n(n+1)/2 entries. */
+int sw_pair_distances(uint32_t n, uint32_t k, const uint32_t* delta, int32_t on_device,
+                      uint32_t* out, size_t cap);
 int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, const uint32_t* word,
                      size_t len, int32_t* result);
 

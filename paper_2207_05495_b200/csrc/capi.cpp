@@ -186,6 +186,23 @@ SW_EXPORT int sw_is_synchronizing(uint32_t n, uint32_t k, const uint32_t* delta,
   return guarded([&] { *result = is_synchronizing(make_aut(n, k, delta)) ? 1 : 0; });
 }
 
+SW_EXPORT int sw_pair_distances(uint32_t n, uint32_t k, const uint32_t* delta, int32_t on_device,
+                                uint32_t* out, size_t cap) {
+  return guarded([&] {
+    const Automaton aut = make_aut(n, k, delta);
+    const size_t need = static_cast<size_t>(n) * (n + 1) / 2;
+    if (cap < need) throw std::invalid_argument("sw_pair_distances: output too small");
+    std::vector<u32> d;
+    if (on_device) {
+      dev::Context ctx(aut);
+      d = dev::pair_distances(ctx, aut);
+    } else {
+      d = pair_merge_distances(aut, InverseTransitions(aut));
+    }
+    std::copy(d.begin(), d.end(), out);
+  });
+}
+
 SW_EXPORT int sw_is_reset_word(uint32_t n, uint32_t k, const uint32_t* delta, const uint32_t* word,
                                size_t len, int32_t* result) {
   return guarded([&] {

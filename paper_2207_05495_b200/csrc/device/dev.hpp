@@ -176,6 +176,10 @@ class Context {
   Scratch scratch_[11];  // slots: kernels.cuh
 };
 
+// ---- pair automaton (pairs.cu): shortest merging word length of every pair
+// {p <= q} at q(q+1)/2 + p, UINT32_MAX when unmergeable (automaton.hpp:119-157)
+std::vector<u32> pair_distances(Context& c, const Automaton& aut);
+
 // ---- list construction / transfer
 DList upload(Context& c, const u64* words, const u32* cards, const u64* tags, size_t count);
 void download(Context& c, const DList& l, u64* words, u32* cards, u64* tags);

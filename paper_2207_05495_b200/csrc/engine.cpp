@@ -954,13 +954,8 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt) {
 }
 
 SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Context* shared) {
-  // Pair merge distances once: the synchronizability precondition
-  // (automaton.hpp:153-157) and Eppstein's bound (heuristics.hpp:26-79) share them.
-  const std::vector<u32> pair_dist = pair_merge_distances(aut, InverseTransitions(aut));
-  if (std::find(pair_dist.begin(), pair_dist.end(), std::numeric_limits<u32>::max()) != pair_dist.end())
-    throw NotSynchronizingError();
   SolveResult res;
-  if (aut.state_count() == 1) {
+  if (aut.state_count() == 1) {  // (synchronizing by definition)
     res.phase = "trivial";
     if (opt.track_word) res.word = Word{};
     return res;
@@ -972,6 +967,16 @@ SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt, dev::Cont
     own = std::make_unique<dev::Context>(aut, opt.device);
   }
   dev::Context& ctx = shared ? *shared : *own;
+  // Pair merge distances once: the synchronizability precondition
+  // (automaton.hpp:153-157) and Eppstein's bound (heuristics.hpp:26-79) share
+  // them.  The pair BFS runs on the device (pairs.cu) from kPairBfsDeviceMin
+  // states on; below that the whole pair graph is a few thousand pairs and the
+  // host's BFS costs less than the launches and readbacks of one level each.
+  const std::vector<u32> pair_dist = aut.state_count() >= kPairBfsDeviceMin
+                                         ? dev::pair_distances(ctx, aut)
+                                         : pair_merge_distances(aut, InverseTransitions(aut));
+  if (std::find(pair_dist.begin(), pair_dist.end(), std::numeric_limits<u32>::max()) != pair_dist.end())
+    throw NotSynchronizingError();
   ctx.timing = opt.timing;
   ctx.contain_stats = opt.contain_stats;
   using clock = std::chrono::steady_clock;

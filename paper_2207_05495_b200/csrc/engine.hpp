@@ -213,6 +213,10 @@ void trace_line(std::ostream* trace, const GpuBibfs& eng, const SearchStats& s, 
 
 }  // namespace detail
 
+// solve_exact computes the pair-merge distances on the device from this many
+// states on (dev::pair_distances), on the host below.
+inline constexpr u32 kPairBfsDeviceMin = 128;
+
 SolveResult solve_exact(const Automaton& aut, const SolveOptions& opt = {});
 // Same, on a caller-owned device context (re-bound to `aut`): a batch worker
 // keeps one context — stream, memory pool, scratch — across its solves.

@@ -27,7 +27,7 @@ STEP_KINDS = ["BFS", "BFS_NH", "IBFS", "IBFS_NH", "DFS"]
 EXPORTED_SYMBOLS = [
     "sw_version", "sw_last_error", "sw_device_count", "sw_default_options",
     "sw_random_automaton", "sw_cerny_automaton", "sw_instance_seed", "sw_parse_automaton",
-    "sw_is_synchronizing", "sw_is_reset_word", "sw_solve_exact", "sw_heuristic",
+    "sw_is_synchronizing", "sw_pair_distances", "sw_is_reset_word", "sw_solve_exact", "sw_heuristic",
     "sw_power_set_oracle", "sw_engine_create", "sw_engine_destroy", "sw_engine_choose",
     "sw_engine_step", "sw_engine_meet", "sw_engine_dfs", "sw_engine_stats_get",
     "sw_list_expand", "sw_list_lex_sort_dedupe", "sw_list_sort_card_desc_lex",
@@ -147,6 +147,8 @@ def load():
     L.sw_parse_automaton.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                      C.c_void_p, C.c_size_t]
     L.sw_is_synchronizing.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(C.c_int32)]
+    L.sw_pair_distances.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_int32, C.c_void_p,
+                                    C.c_size_t]
     L.sw_is_reset_word.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_void_p, C.c_size_t,
                                    C.POINTER(C.c_int32)]
     L.sw_solve_exact.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.POINTER(SolveOptions),
@@ -317,6 +319,15 @@ def is_synchronizing(aut: Automaton) -> bool:
     r = C.c_int32()
     _check(load().sw_is_synchronizing(aut.n, aut.k, aut.delta, C.byref(r)))
     return bool(r.value)
+
+
+def pair_distances(aut: Automaton, on_device: bool = True) -> np.ndarray:
+    """Shortest merging word length of every pair {p <= q} at q(q+1)/2 + p
+    (UINT32_MAX: unmergeable) — automaton.hpp:119-157; on_device: device/pairs.cu."""
+    out = np.zeros(aut.n * (aut.n + 1) // 2, np.uint32)
+    _check(load().sw_pair_distances(aut.n, aut.k, aut.delta, int(on_device),
+                                    out.ctypes.data_as(C.c_void_p), out.size))
+    return out
 
 
 def is_reset_word(aut: Automaton, word: Sequence[int]) -> bool:

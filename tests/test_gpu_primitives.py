@@ -341,3 +341,40 @@ def test_trie_exists_any_key_order(gpu, ref, n, da, db, seed):
         met, ai, bi = gpu.list_trie_exists(n, keys.reshape(-1), b2.reshape(-1))
         assert met
         assert np.all((keys[ai] & ~b2[bi]) == 0)
+
+
+def _two_component(n):
+    """Two disjoint cycles (states < n/2 and >= n/2): no pair across them merges."""
+    h = n // 2
+    d = np.zeros(n * 2, np.uint32)
+    for q in range(n):
+        lo, size = (0, h) if q < h else (h, n - h)
+        d[2 * q] = lo + (q - lo + 1) % size      # rotate inside the component
+        d[2 * q + 1] = lo if q - lo < 2 else q   # merge the component's first two states
+    return d
+
+
+@pytest.mark.parametrize("spec", ["random:50,2,1", "random:300,2,0", "random:570,2,0",
+                                  "random:200,3,1", "cerny:20", "cerny:64", "batch553",
+                                  "split200"])
+def test_pair_distances_device_equals_host(gpu, ref, spec):
+    """The pair-automaton BFS on the GPU (device/pairs.cu) equals the host's
+    level-synchronous BFS entry for entry (automaton.hpp:119-157), including the
+    unmergeable pairs of non-synchronizing automata; solve_exact takes the device
+    table from kPairBfsDeviceMin states on, so a non-synchronizing automaton of
+    200 states must still be refused."""
+    if spec == "batch553":  # config 2's non-synchronizing instance (instance_seed(0,100,553))
+        aut = gpu.random_automaton(100, 2, 16462524638486953121)
+    elif spec == "split200":
+        aut = gpu.Automaton(200, 2, _two_component(200))
+    else:
+        aut = gpu.from_spec(spec)
+    d = gpu.pair_distances(aut, on_device=True)
+    h = gpu.pair_distances(aut, on_device=False)
+    assert np.array_equal(d, h)
+    sync = bool((d != np.iinfo(np.uint32).max).all())
+    assert sync == gpu.is_synchronizing(aut) == bool(ref.is_synchronizing(aut.n, aut.k, aut.delta))
+    if spec == "split200":
+        assert not sync
+        with pytest.raises(gpu.NotSynchronizingError):
+            gpu.solve_exact(aut)
