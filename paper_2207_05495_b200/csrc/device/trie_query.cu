@@ -157,11 +157,14 @@ __global__ void map_flags_kernel(const uint8_t* __restrict__ src, const u32* __r
 #endif
 template <int W>
 constexpr int kTrieSlots = W <= 6 ? 2 : SW_TRIE_SLOTS_WIDE;
+#ifndef SW_TRIE_MINB_WIDE
+#define SW_TRIE_MINB_WIDE 3  // 4 (<= 85 registers) spills at W=9: 4.49 vs 4.33 s (n=570 probe)
+#endif
 #ifndef SW_TRIE_MINB_NARROW
 #define SW_TRIE_MINB_NARROW 4
 #endif
 template <int W, bool PROPER, bool EXIST>
-__global__ void __launch_bounds__(kThreads, (W <= 6 ? SW_TRIE_MINB_NARROW : (W <= 10 ? 3 : 1)))
+__global__ void __launch_bounds__(kThreads, (W <= 6 ? SW_TRIE_MINB_NARROW : (W <= 10 ? SW_TRIE_MINB_WIDE : 1)))
     trie_pool_kernel(
     const u64* __restrict__ K, const ulonglong2* __restrict__ Ksig,
     const TrieNode* __restrict__ nodes, const ulonglong2* __restrict__ psig,
