@@ -341,9 +341,10 @@ constexpr u32 kNone = 0xFFFFFFFFu;
 #define SW_POOL_MINB_WIDE 1
 #endif
 #ifndef SW_POOL_MINB_NARROW
-#define SW_POOL_MINB_NARROW 6
+#define SW_POOL_MINB_NARROW 5
 #endif
-// Resident CTAs per SM: 6 for W <= 6 (56 registers); wider rows need more
+// Resident CTAs per SM: 5 for W <= 6 (64 registers; measured n=300 s0/s1/s2
+// engine 95.5/35.3/85.8 ms against 98.8/36.6/89.1 at 6); wider rows need more
 // registers per lane (the query row, the key row of a leaf).
 constexpr int pool_min_blocks(int W) {
   return W <= 6 ? SW_POOL_MINB_NARROW : (W <= 10 ? SW_POOL_MINB_WIDE : 1);
